@@ -1,0 +1,120 @@
+/*
+ * tsdict_cuda.h -- C ABI of the B200 (sm_100a) tsdict hot path.
+ *
+ * The reference `tsdict` library (/root/reference/proj) is header-only C++;
+ * its hot path sits behind inline functions in namespace tsdict. This C ABI is
+ * what those functions bind to in the drop-in headers under include/tsdict/
+ * (and what a ctypes / cgo / JNI binding would call).
+ * Plain pointers and sizes only; all buffers are caller-owned HOST memory
+ * unless the name says _device. Every entry point is thread-safe (per-thread
+ * stream and scratch) and deterministic.
+ *
+ * Return value: 0 on success, otherwise 1 + the ordinal of tsdict::errc
+ * (reference include/tsdict/errors.hpp:13-35), or TSD_CUDA_ERROR. The message
+ * of the last failure on the calling thread is tsd_last_error().
+ */
+#ifndef TSDICT_CUDA_H
+#define TSDICT_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum tsd_status {
+  TSD_OK = 0,
+  TSD_WINDOW_TOO_SMALL = 1,     /* errc::window_too_small */
+  TSD_WINDOW_TOO_LARGE = 2,     /* errc::window_too_large */
+  TSD_NON_FINITE_INPUT = 3,     /* errc::non_finite_input */
+  TSD_LENGTH_MISMATCH = 4,      /* errc::length_mismatch */
+  TSD_SERIES_TOO_SHORT = 5,     /* errc::series_too_short */
+  TSD_ITERATION_CAP_EXCEEDED = 6,
+  TSD_SOURCE_MISMATCH = 7,      /* errc::source_mismatch */
+  TSD_WINDOW_MISMATCH = 8,      /* errc::window_mismatch */
+  TSD_EMPTY_DICTIONARY = 9,     /* errc::empty_dictionary */
+  TSD_EMPTY_PROFILE = 10,
+  TSD_DEGENERATE_LABELS = 11,
+  TSD_PARSE_ERROR = 12,
+  TSD_VERSION_ERROR = 13,
+  TSD_SCHEMA_ERROR = 14,
+  TSD_IO_ERROR = 15,
+  TSD_INVALID_ARGUMENT = 16,    /* errc::invalid_argument */
+  TSD_CUDA_ERROR = 100          /* device failure (no reference counterpart) */
+};
+
+enum tsd_precision { TSD_FP64 = 0, TSD_FP32 = 1 };
+
+/* Replaces tsdict::compute_stats (series.hpp:83-150). Outputs hold n-m+1
+ * entries: window means, population stds, invn = 1/(std*sqrt(m)) or 0 when
+ * flat, and the flat mask. */
+int tsd_compute_stats(const double* x, size_t n, size_t m, double* means, double* stds, double* invn,
+                      unsigned char* flat);
+
+/* Replaces tsdict::ab_join (profiles.hpp:306-342). val/idx hold na-m+1
+ * entries (distance, nearest window index of b). */
+int tsd_ab_join(const double* a, size_t na, const double* b, size_t nb, size_t m, int precision, double* val,
+                int64_t* idx);
+
+/* Replaces tsdict::self_join (profiles.hpp:266-301) with the exclusion zone as
+ * a parameter: neighbours j with |i-j| <= excl are inadmissible. The
+ * reference uses excl = m/2 (profiles.hpp:273); pass TSD_EXCL_DEFAULT for it. */
+#define TSD_EXCL_DEFAULT ((size_t)-1)
+int tsd_self_join(const double* t, size_t n, size_t m, size_t excl, int precision, double* val, int64_t* idx);
+
+/* Replaces tsdict::detail::dict_min_profile (dictionary.hpp:149-193), the
+ * engine of join_dictionary (dict_join.hpp:42-48) and compute_e_max
+ * (dictionary.hpp:247-255). Segments are packed back to back in seg_vals
+ * (seg_len[s] samples each); seg_start[s] is Segment::start in source
+ * coordinates. One device launch covers every segment; windows straddling
+ * segment boundaries are never formed. idx is in source coordinates. */
+int tsd_dict_join(const double* q, size_t nq, const double* seg_vals, const size_t* seg_len,
+                  const size_t* seg_start, size_t nseg, size_t m, int precision, double* val, int64_t* idx);
+
+/* Batched form (no reference counterpart; equivalent to join_dictionary per
+ * series): nseries query series packed back to back in q_vals (q_len[k]
+ * samples each). Outputs are packed per series: sum_k (q_len[k]-m+1) rows. */
+int tsd_dict_join_batched(const double* q_vals, const size_t* q_len, size_t nseries, const double* seg_vals,
+                          const size_t* seg_len, const size_t* seg_start, size_t nseg, size_t m, int precision,
+                          double* val, int64_t* idx);
+
+/* Replaces tsdict::compute_e_max (dictionary.hpp:247-255): the largest
+ * dictionary-join distance of the source series against its dictionary.
+ * source_length is Dictionary::source_length. */
+int tsd_compute_e_max(const double* t, size_t n, size_t source_length, const double* seg_vals, const size_t* seg_len,
+                      const size_t* seg_start, size_t nseg, size_t m, double* e_max);
+
+/* ---- device-resident plan API (inputs already in HBM; used by bench.py) ---- */
+typedef struct tsd_dict_plan tsd_dict_plan;
+
+/* Uploads a dictionary (host buffers, as tsd_dict_join) once. */
+int tsd_dict_plan_create(const double* seg_vals, const size_t* seg_len, const size_t* seg_start, size_t nseg,
+                         size_t m, int precision, tsd_dict_plan** plan);
+/* Joins device-resident query series (d_q: sum q_len doubles) against the
+ * plan's dictionary; d_val/d_idx are device buffers of sum (q_len-m+1).
+ * `stream` is a cudaStream_t (0 = the plan's own stream). Synchronous. */
+int tsd_dict_plan_join_device(tsd_dict_plan* plan, const double* d_q, const size_t* q_len, size_t nseries,
+                              double* d_val, int64_t* d_idx, void* stream);
+/* Same with host buffers (copies inside). */
+int tsd_dict_plan_join(tsd_dict_plan* plan, const double* q, const size_t* q_len, size_t nseries, double* val,
+                       int64_t* idx);
+int tsd_dict_plan_destroy(tsd_dict_plan* plan);
+/* CUDA-event device times (ms) of the last join call of this plan: the whole
+ * device pipeline (window stats + join + epilogue) and the join kernels
+ * alone, plus the number of kernel launches that call issued. */
+int tsd_dict_plan_last_timing(tsd_dict_plan* plan, double* step_ms, double* join_ms, int* launches);
+
+/* ---- diagnostics ---- */
+const char* tsd_last_error(void);
+const char* tsd_status_name(int status); /* reference errc_name (errors.hpp:37-57) */
+const char* tsd_build_info(void);
+/* Measured DFMA (precision 0) / FFMA (precision 1) throughput of device 0 in
+ * FLOP/s over roughly `seconds` of sustained load. */
+int tsd_measure_peak(int precision, double seconds, double* flops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TSDICT_CUDA_H */

@@ -1,0 +1,136 @@
+// ref_shim.cpp -- ORACLE BUILD ONLY (test infrastructure).
+//
+// Compiles the UNMODIFIED reference headers where they lie under
+// /root/reference/proj (include/tsdict/*.hpp, tests/oracles.hpp,
+// tests/synth.hpp) into oracle/_ref/libtsdict_ref.so and exposes their
+// hot-path entry points through a C ABI for tests/golden/make_golden.py and
+// for bench.py's CPU baseline ("kind": "reference"). Nothing from the
+// reference is copied into this repository; oracle/Makefile points the
+// include path at /root/reference and writes only into oracle/_ref/.
+// <unsupported/Eigen/FFT> comes from oracle/standin (used by MASS only).
+//
+// Status codes: 0 ok, else 1 + tsdict::errc ordinal.
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "oracles.hpp"  // /root/reference/proj/tests/oracles.hpp
+#include "synth.hpp"    // /root/reference/proj/tests/synth.hpp
+#include "tsdict/dict_join.hpp"
+#include "tsdict/dictionary.hpp"
+#include "tsdict/profiles.hpp"
+#include "tsdict/series.hpp"
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const tsdict::error& e) {
+    return 1 + static_cast<int>(e.code());
+  } catch (...) {
+    return 100;
+  }
+}
+
+void emit(const tsdict::MatrixProfile& p, double* val, int64_t* idx) {
+  std::memcpy(val, p.values.data(), p.values.size() * sizeof(double));
+  std::memcpy(idx, p.indices.data(), p.indices.size() * sizeof(int64_t));
+}
+
+tsdict::TimeSeries ts(const double* x, size_t n) { return tsdict::TimeSeries{std::vector<double>(x, x + n)}; }
+
+}  // namespace
+
+extern "C" {
+
+int tsdr_compute_stats(const double* x, size_t n, size_t m, double* means, double* stds, double* invn,
+                       unsigned char* flat) {
+  return guarded([&] {
+    const auto st = tsdict::compute_stats(ts(x, n), m);
+    std::memcpy(means, st.means.data(), st.count() * sizeof(double));
+    std::memcpy(stds, st.stds.data(), st.count() * sizeof(double));
+    std::memcpy(invn, st.invn.data(), st.count() * sizeof(double));
+    std::memcpy(flat, st.constant_mask.data(), st.count());
+  });
+}
+
+int tsdr_ab_join(const double* a, size_t na, const double* b, size_t nb, size_t m, unsigned threads, double* val,
+                 int64_t* idx) {
+  return guarded([&] { emit(tsdict::ab_join(ts(a, na), ts(b, nb), m, threads), val, idx); });
+}
+
+int tsdr_self_join(const double* t, size_t n, size_t m, unsigned threads, double* val, int64_t* idx) {
+  return guarded([&] { emit(tsdict::self_join(ts(t, n), m, threads), val, idx); });
+}
+
+int tsdr_join_dictionary(const double* q, size_t nq, const double* seg_vals, const size_t* seg_len,
+                         const size_t* seg_start, size_t nseg, size_t m, size_t dict_m, unsigned threads,
+                         double* val, int64_t* idx) {
+  return guarded([&] {
+    tsdict::Dictionary D;
+    D.m = dict_m;
+    size_t off = 0, last = 0;
+    for (size_t s = 0; s < nseg; ++s) {
+      tsdict::Segment seg;
+      seg.start = seg_start[s];
+      seg.values.assign(seg_vals + off, seg_vals + off + seg_len[s]);
+      off += seg_len[s];
+      last = seg_start[s] + seg_len[s];
+      D.segments.push_back(std::move(seg));
+    }
+    D.source_length = last;
+    emit(tsdict::join_dictionary(ts(q, nq), D, m, threads), val, idx);
+  });
+}
+
+int tsdr_compute_e_max(const double* t, size_t n, const double* seg_vals, const size_t* seg_len,
+                       const size_t* seg_start, size_t nseg, size_t m, unsigned threads, double* out) {
+  return guarded([&] {
+    tsdict::Dictionary D;
+    D.m = m;
+    D.source_length = n;
+    size_t off = 0;
+    for (size_t s = 0; s < nseg; ++s) {
+      tsdict::Segment seg;
+      seg.start = seg_start[s];
+      seg.values.assign(seg_vals + off, seg_vals + off + seg_len[s]);
+      off += seg_len[s];
+      D.segments.push_back(std::move(seg));
+    }
+    *out = tsdict::compute_e_max(D, ts(t, n), threads);
+  });
+}
+
+// tests/oracles.hpp long-double brute force
+int tsdr_ab_join_brute(const double* a, size_t na, const double* b, size_t nb, size_t m, double* val,
+                       int64_t* idx) {
+  return guarded([&] {
+    emit(oracle::ab_join_brute(std::vector<double>(a, a + na), std::vector<double>(b, b + nb), m), val, idx);
+  });
+}
+
+int tsdr_self_join_brute(const double* t, size_t n, size_t m, double* val, int64_t* idx) {
+  return guarded([&] { emit(oracle::self_join_brute(std::vector<double>(t, t + n), m), val, idx); });
+}
+
+// tests/synth.hpp generators, so fixtures replay the reference tests' own draws
+void* tsdr_rng_new(uint64_t seed) { return new synth::rng_t(seed); }
+void tsdr_rng_free(void* h) { delete static_cast<synth::rng_t*>(h); }
+void tsdr_noise(void* h, size_t n, double* out) {
+  const auto v = synth::noise(*static_cast<synth::rng_t*>(h), n);
+  std::memcpy(out, v.data(), n * sizeof(double));
+}
+void tsdr_walk(void* h, size_t n, double* out) {
+  const auto v = synth::walk(*static_cast<synth::rng_t*>(h), n);
+  std::memcpy(out, v.data(), n * sizeof(double));
+}
+void tsdr_sine(size_t n, double period, double amp, double* out) {
+  const auto v = synth::sine(n, period, amp);
+  std::memcpy(out, v.data(), n * sizeof(double));
+}
+
+}  // extern "C"

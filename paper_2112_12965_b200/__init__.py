@@ -1,0 +1,360 @@
+"""tsdict-b200: the reference `tsdict` hot path on B200 (sm_100a).
+
+Python mirror of the reference C++ API (namespace ``tsdict``, reference
+proj/include/tsdict/*.hpp) over the C ABI in ``include/tsdict_cuda.h``
+(built in-tree as ``libtsdict_cuda.so``). Same function names, argument
+meaning and error behaviour: failures raise :class:`TsdictError` whose
+``code`` is the reference ``tsdict::errc`` (errors.hpp:13-35) and whose
+message is prefixed by the code name (errors.hpp:59-62).
+
+There is no CPU fallback: every compute call runs the CUDA library and
+raises if it is missing or no GPU is present.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtsdict_cuda.so")
+
+__all__ = [
+    "errc", "TsdictError", "TimeSeries", "SubseqStats", "MatrixProfile", "Segment", "Dictionary",
+    "compute_stats", "ab_join", "self_join", "join_dictionary", "dict_min_profile", "compute_e_max",
+    "join_dictionary_batched", "corr_to_dist", "DictPlan", "load_library", "measure_peak", "build_info",
+    "C_SYMBOLS",
+]
+
+
+class errc(enum.IntEnum):
+    """reference errors.hpp:13-35 (ordinal order preserved)."""
+    window_too_small = 0
+    window_too_large = 1
+    non_finite_input = 2
+    length_mismatch = 3
+    series_too_short = 4
+    iteration_cap_exceeded = 5
+    source_mismatch = 6
+    window_mismatch = 7
+    empty_dictionary = 8
+    empty_profile = 9
+    degenerate_labels = 10
+    parse_error = 11
+    version_error = 12
+    schema_error = 13
+    io_error = 14
+    invalid_argument = 15
+    cuda_error = 99  # device failure; no reference counterpart
+
+
+_ERRC_NAME = {
+    errc.window_too_small: "WindowTooSmall", errc.window_too_large: "WindowTooLarge",
+    errc.non_finite_input: "NonFiniteInput", errc.length_mismatch: "LengthMismatch",
+    errc.series_too_short: "SeriesTooShort", errc.iteration_cap_exceeded: "IterationCapExceeded",
+    errc.source_mismatch: "SourceMismatch", errc.window_mismatch: "WindowMismatch",
+    errc.empty_dictionary: "EmptyDictionary", errc.empty_profile: "EmptyProfile",
+    errc.degenerate_labels: "DegenerateLabels", errc.parse_error: "ParseError",
+    errc.version_error: "VersionError", errc.schema_error: "SchemaError", errc.io_error: "IoError",
+    errc.invalid_argument: "InvalidArgument", errc.cuda_error: "CudaError",
+}
+
+
+class TsdictError(RuntimeError):
+    """reference tsdict::error (errors.hpp:59-68): what() = '<CodeName>: message'."""
+
+    def __init__(self, code: errc, message: str):
+        self._code = errc(code)
+        text = message if message.startswith(_ERRC_NAME[self._code] + ":") else f"{_ERRC_NAME[self._code]}: {message}"
+        super().__init__(text)
+
+    def code(self) -> errc:
+        return self._code
+
+
+# ---------------------------------------------------------------------------
+# library loading
+# ---------------------------------------------------------------------------
+_f64p = ctypes.POINTER(ctypes.c_double)
+_i64p = ctypes.POINTER(ctypes.c_int64)
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+_szp = ctypes.POINTER(ctypes.c_size_t)
+_sz = ctypes.c_size_t
+_int = ctypes.c_int
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes); every symbol include/tsdict_cuda.h declares
+C_SYMBOLS = {
+    "tsd_compute_stats": (_int, [_f64p, _sz, _sz, _f64p, _f64p, _f64p, _u8p]),
+    "tsd_ab_join": (_int, [_f64p, _sz, _f64p, _sz, _sz, _int, _f64p, _i64p]),
+    "tsd_self_join": (_int, [_f64p, _sz, _sz, _sz, _int, _f64p, _i64p]),
+    "tsd_dict_join": (_int, [_f64p, _sz, _f64p, _szp, _szp, _sz, _sz, _int, _f64p, _i64p]),
+    "tsd_dict_join_batched": (_int, [_f64p, _szp, _sz, _f64p, _szp, _szp, _sz, _sz, _int, _f64p, _i64p]),
+    "tsd_compute_e_max": (_int, [_f64p, _sz, _sz, _f64p, _szp, _szp, _sz, _sz, _f64p]),
+    "tsd_dict_plan_create": (_int, [_f64p, _szp, _szp, _sz, _sz, _int, ctypes.POINTER(_vp)]),
+    "tsd_dict_plan_join_device": (_int, [_vp, _vp, _szp, _sz, _vp, _vp, _vp]),
+    "tsd_dict_plan_join": (_int, [_vp, _f64p, _szp, _sz, _f64p, _i64p]),
+    "tsd_dict_plan_destroy": (_int, [_vp]),
+    "tsd_dict_plan_last_timing": (_int, [_vp, _f64p, _f64p, ctypes.POINTER(_int)]),
+    "tsd_last_error": (ctypes.c_char_p, []),
+    "tsd_status_name": (ctypes.c_char_p, [_int]),
+    "tsd_build_info": (ctypes.c_char_p, []),
+    "tsd_measure_peak": (_int, [_int, ctypes.c_double, _f64p]),
+}
+
+_lib = None
+
+
+def load_library() -> ctypes.CDLL:
+    """Load libtsdict_cuda.so (built by __graft_entry__.build()). Raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise TsdictError(errc.cuda_error, f"CUDA library not built: {LIB_PATH} (run __graft_entry__.build())")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in C_SYMBOLS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = load_library().tsd_last_error().decode(errors="replace")
+        code = errc.cuda_error if rc == 100 else errc(rc - 1)
+        raise TsdictError(code, msg)
+
+
+def _f64(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+def _ptr(a: np.ndarray, typ):
+    return a.ctypes.data_as(typ)
+
+
+_PREC = {"fp64": 0, "fp32": 1, 0: 0, 1: 1}
+
+
+# ---------------------------------------------------------------------------
+# types (series.hpp:27-45, profiles.hpp:44-51, dictionary.hpp:46-68)
+# ---------------------------------------------------------------------------
+@dataclass
+class TimeSeries:
+    values: np.ndarray
+
+    def __post_init__(self):
+        self.values = _f64(self.values)
+
+    def n(self) -> int:
+        return int(self.values.size)
+
+
+def _vals(T) -> np.ndarray:
+    return T.values if isinstance(T, TimeSeries) else _f64(T)
+
+
+@dataclass
+class SubseqStats:
+    m: int
+    means: np.ndarray
+    stds: np.ndarray
+    invn: np.ndarray
+    constant_mask: np.ndarray
+
+    def count(self) -> int:
+        return int(self.means.size)
+
+
+@dataclass
+class MatrixProfile:
+    no_neighbor = -1
+    values: np.ndarray
+    indices: np.ndarray
+    kind: str = "self"
+    m: int = 0
+
+
+@dataclass
+class Segment:
+    start: int
+    values: np.ndarray
+
+    def __post_init__(self):
+        self.values = _f64(self.values)
+
+    def length(self) -> int:
+        return int(self.values.size)
+
+
+@dataclass
+class Dictionary:
+    segments: List[Segment] = field(default_factory=list)
+    m: int = 0
+    k: float = 1.5
+    source_length: int = 0
+    core_starts: List[int] = field(default_factory=list)
+    e_max: Optional[float] = None
+    space_saving: float = 0.0
+    no_progress: bool = False
+
+    def stored_samples(self) -> int:
+        return sum(s.length() for s in self.segments)
+
+
+def _pack_dict(D: Dictionary):
+    lens = np.asarray([s.length() for s in D.segments], dtype=np.uintp)
+    starts = np.asarray([s.start for s in D.segments], dtype=np.uintp)
+    vals = _f64(np.concatenate([s.values for s in D.segments])) if D.segments else np.zeros(1)
+    return vals, lens, starts
+
+
+# ---------------------------------------------------------------------------
+# hot-path API
+# ---------------------------------------------------------------------------
+def corr_to_dist(rho: float, m: int) -> float:
+    """series.hpp:153-161 (host helper)."""
+    rho = min(1.0, max(-1.0, rho))
+    d = float(np.sqrt(2.0 * m * (1.0 - rho)))
+    return min(max(d, 0.0), 2.0 * float(np.sqrt(m)))
+
+
+def compute_stats(T, m: int) -> SubseqStats:
+    """series.hpp:83-150."""
+    x = _vals(T)
+    lib = load_library()
+    cnt = max(0, x.size - m + 1)
+    means, stds, invn = (np.empty(max(cnt, 1)) for _ in range(3))
+    flat = np.empty(max(cnt, 1), dtype=np.uint8)
+    _check(lib.tsd_compute_stats(_ptr(x, _f64p), x.size, m, _ptr(means, _f64p), _ptr(stds, _f64p),
+                                 _ptr(invn, _f64p), _ptr(flat, _u8p)))
+    return SubseqStats(m, means[:cnt], stds[:cnt], invn[:cnt], flat[:cnt])
+
+
+def ab_join(A, B, m: int, threads: int = 0, precision="fp64") -> MatrixProfile:
+    """profiles.hpp:306-342. `threads` is accepted for API parity and ignored."""
+    a, b = _vals(A), _vals(B)
+    lib = load_library()
+    cnt = max(1, a.size - m + 1)
+    val, idx = np.empty(cnt), np.empty(cnt, dtype=np.int64)
+    _check(lib.tsd_ab_join(_ptr(a, _f64p), a.size, _ptr(b, _f64p), b.size, m, _PREC[precision],
+                           _ptr(val, _f64p), _ptr(idx, _i64p)))
+    return MatrixProfile(val, idx, "ab", m)
+
+
+def self_join(T, m: int, threads: int = 0, excl: Optional[int] = None, precision="fp64") -> MatrixProfile:
+    """profiles.hpp:266-301; `excl` defaults to the reference's m // 2 (:273)."""
+    x = _vals(T)
+    lib = load_library()
+    cnt = max(1, x.size - m + 1)
+    val, idx = np.empty(cnt), np.empty(cnt, dtype=np.int64)
+    e = ctypes.c_size_t(-1).value if excl is None else int(excl)
+    _check(lib.tsd_self_join(_ptr(x, _f64p), x.size, m, e, _PREC[precision], _ptr(val, _f64p), _ptr(idx, _i64p)))
+    return MatrixProfile(val, idx, "self", m)
+
+
+def dict_min_profile(T, D: Dictionary, m: int, threads: int = 0, precision="fp64") -> MatrixProfile:
+    """dictionary.hpp:149-193 (detail::dict_min_profile)."""
+    q = _vals(T)
+    vals, lens, starts = _pack_dict(D)
+    lib = load_library()
+    cnt = max(1, q.size - m + 1)
+    val, idx = np.empty(cnt), np.empty(cnt, dtype=np.int64)
+    _check(lib.tsd_dict_join(_ptr(q, _f64p), q.size, _ptr(vals, _f64p), _ptr(lens, _szp), _ptr(starts, _szp),
+                             len(D.segments), m, _PREC[precision], _ptr(val, _f64p), _ptr(idx, _i64p)))
+    return MatrixProfile(val, idx, "ab", m)
+
+
+def join_dictionary(A, D: Dictionary, m: int, threads: int = 0, precision="fp64") -> MatrixProfile:
+    """dict_join.hpp:42-48."""
+    if m != D.m:
+        raise TsdictError(errc.window_mismatch, "requested window length differs from the dictionary's")
+    return dict_min_profile(A, D, m, threads, precision)
+
+
+def join_dictionary_batched(series: Sequence, D: Dictionary, m: int, precision="fp64") -> List[MatrixProfile]:
+    """join_dictionary over many query series in one device pass (BASELINE C5)."""
+    if m != D.m:
+        raise TsdictError(errc.window_mismatch, "requested window length differs from the dictionary's")
+    qs = [_vals(s) for s in series]
+    qlen = np.asarray([q.size for q in qs], dtype=np.uintp)
+    q = _f64(np.concatenate(qs))
+    vals, lens, starts = _pack_dict(D)
+    lib = load_library()
+    cnts = [max(0, int(n) - m + 1) for n in qlen]
+    tot = max(1, sum(cnts))
+    val, idx = np.empty(tot), np.empty(tot, dtype=np.int64)
+    _check(lib.tsd_dict_join_batched(_ptr(q, _f64p), _ptr(qlen, _szp), len(qs), _ptr(vals, _f64p),
+                                     _ptr(lens, _szp), _ptr(starts, _szp), len(D.segments), m, _PREC[precision],
+                                     _ptr(val, _f64p), _ptr(idx, _i64p)))
+    out, o = [], 0
+    for c in cnts:
+        out.append(MatrixProfile(val[o:o + c], idx[o:o + c], "ab", m))
+        o += c
+    return out
+
+
+def compute_e_max(D: Dictionary, T_B, threads: int = 0) -> float:
+    """dictionary.hpp:247-255."""
+    x = _vals(T_B)
+    vals, lens, starts = _pack_dict(D)
+    lib = load_library()
+    out = ctypes.c_double(0.0)
+    _check(lib.tsd_compute_e_max(_ptr(x, _f64p), x.size, D.source_length, _ptr(vals, _f64p), _ptr(lens, _szp),
+                                 _ptr(starts, _szp), len(D.segments), D.m, ctypes.byref(out)))
+    return out.value
+
+
+class DictPlan:
+    """Dictionary resident in HBM; joins device-resident queries (bench path)."""
+
+    def __init__(self, D: Dictionary, m: int, precision="fp64"):
+        vals, lens, starts = _pack_dict(D)
+        self._lib = load_library()
+        self._h = ctypes.c_void_p()
+        self.m = m
+        _check(self._lib.tsd_dict_plan_create(_ptr(vals, _f64p), _ptr(lens, _szp), _ptr(starts, _szp),
+                                              len(D.segments), m, _PREC[precision], ctypes.byref(self._h)))
+
+    def join_device(self, d_q: int, q_len: Sequence[int], d_val: int, d_idx: int, stream: int = 0) -> None:
+        ql = np.asarray(q_len, dtype=np.uintp)
+        _check(self._lib.tsd_dict_plan_join_device(self._h, ctypes.c_void_p(d_q), _ptr(ql, _szp), len(ql),
+                                                   ctypes.c_void_p(d_val), ctypes.c_void_p(d_idx),
+                                                   ctypes.c_void_p(stream)))
+
+    def join_host(self, q: np.ndarray, q_len: Sequence[int], val: np.ndarray, idx: np.ndarray) -> None:
+        ql = np.asarray(q_len, dtype=np.uintp)
+        _check(self._lib.tsd_dict_plan_join(self._h, _ptr(q, _f64p), _ptr(ql, _szp), len(ql), _ptr(val, _f64p),
+                                            _ptr(idx, _i64p)))
+
+    def last_timing(self):
+        s, j, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+        _check(self._lib.tsd_dict_plan_last_timing(self._h, ctypes.byref(s), ctypes.byref(j), ctypes.byref(n)))
+        return s.value, j.value, n.value
+
+    def close(self):
+        if self._h:
+            self._lib.tsd_dict_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def measure_peak(precision="fp64", seconds: float = 1.0) -> float:
+    out = ctypes.c_double()
+    _check(load_library().tsd_measure_peak(_PREC[precision], seconds, ctypes.byref(out)))
+    return out.value
+
+
+def build_info() -> str:
+    return load_library().tsd_build_info().decode()

@@ -1,0 +1,121 @@
+// tsd_internal.h -- host-side interfaces between the C ABI (capi.cu) and the
+// kernel modules (stats.cu, join.cu, selfjoin.cu). Not installed.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace tsd {
+
+// Status codes: 0 ok, else 1 + tsdict::errc ordinal (reference errors.hpp:13-35).
+enum Status : int {
+  kOk = 0,
+  kWindowTooSmall = 1,
+  kWindowTooLarge = 2,
+  kNonFiniteInput = 3,
+  kLengthMismatch = 4,
+  kSeriesTooShort = 5,
+  kIterationCapExceeded = 6,
+  kSourceMismatch = 7,
+  kWindowMismatch = 8,
+  kEmptyDictionary = 9,
+  kEmptyProfile = 10,
+  kDegenerateLabels = 11,
+  kInvalidArgument = 16,
+  kCudaError = 100,
+};
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+// One window-statistics "threshold group": windows [wbeg, wend) of a
+// concatenated sample buffer that belong to one reference TimeSeries (or one
+// 16384-window query block of it, dictionary.hpp:175-180); the constancy
+// threshold (series.hpp:75-77) uses max|x| over samples [wbeg, wend-1+m).
+struct Group {
+  int64_t wbeg, wend;
+  int32_t series;  // index into the caller's series list (non-finite reporting order)
+  int32_t pad;
+};
+
+// Device arrays describing every window of a concatenated sample buffer.
+// flag bit 0: window lies inside one series (valid); bit 1: window is flat.
+struct WindowArrays {
+  int64_t nwin = 0;
+  double* mu = nullptr;
+  double* sd = nullptr;
+  double* invn = nullptr;
+  double* df = nullptr;
+  double* dg = nullptr;
+  uint8_t* flag = nullptr;
+};
+
+// Dictionary segment as laid out on the device: its window 0 is concatenated
+// column col0; ncol valid windows; src0 = Segment::start (dictionary.hpp:46-51).
+struct SegDev {
+  int64_t col0;
+  int64_t src0;
+  int32_t ncol;
+  int32_t pad;
+};
+
+// Scratch arena: a list of device blocks handed out bump-style; reset()
+// rewinds without freeing so repeated calls of the same shape do not hit
+// cudaMalloc. Grows, never shrinks.
+struct Arena {
+  struct Blk {
+    char* p;
+    size_t cap, used;
+  };
+  std::vector<Blk> blks;
+  size_t cur = 0;
+  ~Arena();
+  void reset() {
+    for (auto& b : blks) b.used = 0;
+    cur = 0;
+  }
+  void* get(size_t bytes);  // nullptr on allocation failure
+};
+
+// stats.cu -------------------------------------------------------------------
+// Computes window arrays for the concatenated buffer d_x[0..n). `bad_series`
+// receives (host) the lowest series index holding a non-finite sample, or -1.
+int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group>& groups, int nseries,
+                    WindowArrays& out, Arena& arena, cudaStream_t st, int* bad_series, Error* err);
+
+// join.cu --------------------------------------------------------------------
+struct JoinInputs {
+  // rows: windows of the concatenated query buffer
+  const double* xa;
+  int64_t na;
+  WindowArrays rows;
+  // columns: windows of the concatenated dictionary buffer
+  const double* xb;
+  int64_t nb;
+  WindowArrays cols;
+  std::vector<SegDev> segs;  // host copy
+  int m;
+  int64_t excl = -1;  // self-join exclusion half-width (|i-j| <= excl rejected); -1 = AB join
+  int precision;      // 0 fp64, 1 fp32
+};
+
+// Runs the row-band join of every row against every valid column of every
+// segment. Writes per-row best (corr, concat column) into d_best_c/d_best_j.
+int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st,
+             Error* err, int* launches);
+
+// Epilogue: corr -> distance (series.hpp:153-161), concat column -> source
+// coordinate (dictionary.hpp:183-188), (inf, -1) sentinel for rows without an
+// admissible neighbour (profiles.hpp:149-151), row compaction for batched
+// queries: series q's valid windows start at row d_woff[q] and are written
+// from output slot d_ooff[q] on (nser == 1: identity).
+int run_epilogue(const double* d_best_c, const int64_t* d_best_j, const uint8_t* d_row_flag, int64_t nrows,
+                 const SegDev* d_segs, int nseg, int m, const int64_t* d_woff, const int64_t* d_ooff, int nser,
+                 double* d_val, int64_t* d_idx, cudaStream_t st, Error* err);
+
+}  // namespace tsd
