@@ -212,8 +212,8 @@ int plan_join_dev(tsd_dict_plan* p, const double* d_q, const size_t* q_len, size
   TRY(run_join(in, d_bc, d_bj, ar, st, &er, &launches));
   CK(cudaEventRecord(p->s.ev[2], st));
   TRY(run_epilogue(d_bc, d_bj, in.rows.flag, nrows, p->d_segs, (int)p->segs.size(), m, d_woff, d_ooff, (int)nser,
-                   d_val, d_idx, st, &er));
-  ++launches;
+                   p->cols.flag, p->cols.nwin, -1, d_val, d_idx, ar, st, &er));
+  launches += 3;
   CK(cudaEventRecord(p->s.ev[3], st));
   CK(cudaEventSynchronize(p->s.ev[3]));
   float a = 0, b = 0;
@@ -335,7 +335,8 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
   CK(cudaMemcpyAsync(d_segs, in.segs.data(), sizeof(SegDev), cudaMemcpyHostToDevice, st));
   int launches = 0;
   TRY(run_join(in, d_bc, d_bj, tc.arena, st, &er, &launches));
-  TRY(run_epilogue(d_bc, d_bj, in.rows.flag, nrows, d_segs, 1, (int)m, nullptr, nullptr, 1, d_val, d_idx, st, &er));
+  TRY(run_epilogue(d_bc, d_bj, in.rows.flag, nrows, d_segs, 1, (int)m, nullptr, nullptr, 1, in.cols.flag, in.cols.nwin,
+                   excl, d_val, d_idx, tc.arena, st, &er));
   CK(cudaMemcpyAsync(val, d_val, sizeof(double) * nrows, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(idx, d_idx, sizeof(int64_t) * nrows, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

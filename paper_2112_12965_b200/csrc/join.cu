@@ -1,36 +1,39 @@
-// join.cu -- z-normalised AB / dictionary join on sm_100a (FP64 path).
+// join.cu -- z-normalised AB / dictionary / self join on sm_100a (FP64 path).
 //
 // Reference semantics: profiles.hpp:306-342 (ab_join) driven per segment by
-// dictionary.hpp:149-193 (dict_min_profile). For every query window i and
+// dictionary.hpp:149-193 (dict_min_profile), and profiles.hpp:266-301
+// (self_join, exclusion zone as a parameter). For every query window i and
 // every valid dictionary window j (never straddling a segment boundary):
 //   cov(i,j) = cov(i-1,j-1) + df_a[i]*dg_b[j] + dg_a[i]*df_b[j]   (profiles.hpp:330)
 //   c = clamp(cov * invn_a[i] * invn_b[j])                         (:331-336)
 //   row best: higher c wins, ties -> lower j                        (:70-77)
 //
 // B200 design:
-//   * a warp owns a BAND of 256 consecutive query rows (8 per lane, "slots")
-//     and sweeps the columns of every segment of its segment group. At step k
-//     all lanes work on column k, so column data is a warp-uniform smem
-//     broadcast and each slot's row data lives in registers for the whole
-//     sweep. The diagonal recurrence moves one slot down per step (register
-//     renaming, no moves) and crosses lanes with one shfl.up per step;
+//   * a warp owns a BAND of 32*R consecutive query rows (R per lane,
+//     "slots") and sweeps the columns of every segment of its segment group.
+//     At step k all lanes work on column k, so column data is a warp-uniform
+//     smem broadcast and each slot's row data lives in registers for the
+//     whole sweep. The diagonal recurrence moves one slot down per step
+//     (register renaming, no moves) and crosses lanes with one shfl.up;
 //   * lane 0's incoming diagonal comes from the bottom row of the band above
 //     (edge buffer, staged through a 3-block smem ring with cp.async); lane 31
 //     writes this band's bottom row back in place;
 //   * diagonals entering a segment at its column 0 start from an exact head
 //     (window_dot, profiles.hpp:101-108) computed as a register-blocked
-//     sliding dot product; the first band of a task also computes the top
-//     edge this way;
-//   * per cell the FP64 pipe does 2 DFMA (update) + 1 DMUL (K = cov*invn_b);
-//     the row test is one integer compare of K's high word against a
-//     per-row threshold derived from the best K so far (conservative by one
-//     high-word ulp). Only when some lane passes does the warp take the exact
-//     slow path, which re-evaluates c exactly as the reference does and
-//     applies the lexicographic rule. Row bests persist for the whole band
-//     sweep, so after a short warm-up the slow path is rare.
+//     sliding dot product; the first band of a task computes the top edge
+//     the same way;
+//   * per cell the FP64 pipe does 2 DFMA (update) + 1 DMUL (K = cov*invn_b,
+//     the row-constant invn_a factored out); the row test is ONE integer
+//     compare of K's high word against a per-row threshold (high word of the
+//     best K so far, minus one, so the test is conservative). Only when some
+//     lane passes does the warp run the exact update (full-precision compare
+//     of K, lowest column on ties since columns arrive in increasing order).
+//     Flat rows (invn_a == 0) are resolved in the epilogue from the flat
+//     column table (profiles.hpp:332-336 gives them c in {0, 1}).
+#include <algorithm>
 #include <climits>
 #include <cstdio>
-#include <algorithm>
+#include <cstdlib>
 
 #include "tsd_common.cuh"
 #include "tsd_internal.h"
@@ -39,12 +42,22 @@ namespace tsd {
 
 namespace {
 
-constexpr int R = 8;        // rows per lane
-constexpr int H = 32 * R;   // rows per band
-constexpr int WARPS = 4;    // warps per CTA
-constexpr int T = 128;      // head staging chunk
-__host__ __device__ constexpr int padidx(int i) { return i + (i >> 3); }
-constexpr int SLIDE = padidx(H + T) + 8;
+constexpr int WARPS = 2;  // warps per CTA (independent; small CTAs give finer occupancy steps)
+constexpr int T = 128;    // head staging chunk (samples)
+#ifndef TSD_JOIN_MINB
+#define TSD_JOIN_MINB 8  // 8 CTAs x 2 warps per SM: caps registers at 128
+#endif
+
+template <int R>
+__host__ __device__ constexpr int padidx(int i) {
+  return i + i / R;  // one pad double per R: lane-strided R-wide windows are bank-conflict free
+}
+
+template <int R>
+struct Geo {
+  static constexpr int H = 32 * R;  // rows per band
+  static constexpr int SLIDE = padidx<R>(32 * R + T) + R;
+};
 
 struct JoinArgs {
   const double* xa;
@@ -62,7 +75,7 @@ struct JoinArgs {
   const double* btil;   // [nseg][m] centred samples of each segment's window 0
   const double* ebt;    // [nseg] sum of btil
   int m;
-  long long excl;
+  long long excl;  // self-join exclusion half-width (SELF kernels only)
   int nbands, bands_per_task, ngroups, ntasks;
   const int* group_seg;  // [ngroups+1]
   int64_t ecap;          // per-warp edge capacity (doubles)
@@ -71,16 +84,14 @@ struct JoinArgs {
   int64_t* out_j;
 };
 
+template <int R>
 struct __align__(16) WarpSmem {
-  double4 colbuf[2][32];
+  double4 colbuf[3][32];
   double ering[96];
   double edummy[96];  // lanes 0..30 store here so lane 31's edge store needs no branch
-  double scov[R][32];  // slow-path scratch: this step's covariances
-  int sthr[R][32];     // slow-path scratch: thresholds
-  double best_c[R][32];
-  long long best_j[R][32];
-  double ivan[R][32];
-  double slide[SLIDE];
+  double bK[R][32];   // best K per slot (exact compare in the update path)
+  int bj[R][32];      // its concatenated column
+  double slide[Geo<R>::SLIDE];
   double unif[T];
 };
 
@@ -93,101 +104,6 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-// out[r] = sum_{t<m} U[t] * (S[8*lane + r + t] - cS), U[t] = Ug[t] - cu.
-// S samples at index >= s_avail read as cS (contribute 0). Returns sum U in *esum.
-__device__ void sliding_dot(WarpSmem& sm, const double* __restrict__ Ug, double cu, const double* __restrict__ Sg,
-                            int64_t s_avail, double cS, int m, int lane, double (&out)[R], double* esum) {
-#pragma unroll
-  for (int r = 0; r < R; ++r) out[r] = 0.0;
-  double es = 0.0;
-  const int base = R * lane;
-  for (int t0 = 0; t0 < m; t0 += T) {
-    const int tl = min(T, m - t0);
-    __syncwarp();
-    for (int q = lane; q < tl; q += 32) {
-      const double u = Ug[t0 + q] - cu;
-      sm.unif[q] = u;
-      es += u;
-    }
-    for (int q = lane; q < H + tl; q += 32) {
-      const int64_t gi = (int64_t)t0 + q;
-      sm.slide[padidx(q)] = gi < s_avail ? Sg[gi] - cS : 0.0;
-    }
-    __syncwarp();
-    double w[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) w[r] = sm.slide[padidx(base + r)];
-    int t = 0;
-    for (; t + R <= tl; t += R) {
-#pragma unroll
-      for (int u = 0; u < R; ++u) {
-        const double uv = sm.unif[t + u];
-#pragma unroll
-        for (int r = 0; r < R; ++r) out[r] = __fma_rn(w[(r + u) & (R - 1)], uv, out[r]);
-        w[u] = sm.slide[padidx(base + t + u + R)];
-      }
-    }
-    // remainder (tl not a multiple of R): w[] holds S[base + t + (0..R-1)] in rotated order
-    for (; t < tl; ++t) {
-      const double uv = sm.unif[t];
-#pragma unroll
-      for (int r = 0; r < R; ++r) out[r] = __fma_rn(sm.slide[padidx(base + t + r)], uv, out[r]);
-    }
-  }
-  if (esum) {
-    for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
-    *esum = es;
-  }
-}
-
-struct SweepCtx {
-  const double4* colg;  // global column data of this segment (col0 aligned)
-  double* E;            // global edge array of this segment (j = 0 .. ncol-2)
-  int ncol;
-  int64_t colbase;  // concatenated column index of this segment's window 0
-  long long row0;   // row of this lane's slot 0
-  long long excl;   // self-join exclusion half-width, -1 for AB joins
-  bool write_out;
-};
-
-// Slow path (taken by the whole warp when any lane's coarse test passed):
-// exact reference evaluation and lexicographic update for every slot whose
-// high-word test passed. Flat rows (invn_a == 0) follow profiles.hpp:332-336:
-// c = 1 against a flat column, else clamp(cov*0*invn_b) = 0. The self-join
-// exclusion zone |i - j| <= excl (profiles.hpp:273, :281-284) is rejected
-// here. Kept out of line: it is rare after warm-up and would otherwise
-// bloat every unrolled step.
-__device__ __noinline__ void slow_all(WarpSmem& sm, int lane, double ivb, long long col, long long row0,
-                                      long long excl) {
-  for (int r = 0; r < R; ++r) {
-    const double cov = sm.scov[r][lane];
-    const double K = cov * ivb;
-    const int thr = sm.sthr[r][lane];
-    if (__double2hiint(K) < thr) continue;
-    const long long row = row0 + r;
-    if (excl >= 0 && (row - col <= excl && col - row <= excl)) continue;
-    const double ia = sm.ivan[r][lane];
-    double c;
-    if (ia == 0.0) {
-      c = ivb == 0.0 ? 1.0 : clamp_corr(cov * ia * ivb);
-    } else {
-      c = clamp_corr(cov * ia * ivb);  // profiles.hpp:331, :335
-    }
-    if (c > sm.best_c[r][lane]) {  // columns arrive in increasing order: ties never win
-      sm.best_c[r][lane] = c;
-      sm.best_j[r][lane] = col;
-      int nt;
-      if (ia == 0.0) {
-        nt = c == 1.0 ? INT_MAX : INT_MIN;
-      } else {
-        const int h = __double2hiint(K);
-        nt = h >= 0 ? h - 1 : INT_MIN;
-      }
-      sm.sthr[r][lane] = nt;
-    }
-  }
 }
 
 __device__ __forceinline__ double shfl_up1(double v) {
@@ -206,121 +122,267 @@ __device__ __forceinline__ bool vote_any(bool p) {
   return r != 0;
 }
 
-template <bool FIRST, bool GUARD>
-__device__ __forceinline__ void sweep_block(WarpSmem& sm, const SweepCtx& cx, int lane, int k0, double (&P)[R],
-                                            const double (&dfa)[R], const double (&dga)[R], int (&thr)[R],
-                                            const double (&head)[R]) {
-  const int cslot = (k0 >> 5) & 1, ci = k0 & 31;
-  const double* eprev = &sm.ering[(k0 + 95) % 96];  // E[k0-1]
-  const double* ecur = &sm.ering[k0 % 96];          // E[k0 .. k0+6]
-  // lane 31 stores into the ring, the others into a dummy copy of it
-  double* sprev = (lane == 31 ? sm.ering : sm.edummy) + (k0 + 95) % 96;
-  double* scur = (lane == 31 ? sm.ering : sm.edummy) + k0 % 96;
-  const bool l0 = lane == 0;
+// out[r] = sum_{t<m} U[t] * (S[R*lane + r + t] - cS), U[t] = Ug[t] - cu.
+// S samples at index >= s_avail read as cS (contribute 0). Returns sum U in *esum.
+template <int R>
+__device__ void sliding_dot(WarpSmem<R>& sm, const double* __restrict__ Ug, double cu, const double* __restrict__ Sg,
+                            int64_t s_avail, double cS, int m, int lane, double (&out)[R], double* esum) {
+  constexpr int H = Geo<R>::H;
 #pragma unroll
-  for (int u = 0; u < R; ++u) {
-    const int k = k0 + u;
-    if (GUARD && k >= cx.ncol) break;
-    const double2 dd = *reinterpret_cast<const double2*>(&sm.colbuf[cslot][ci + u]);
-    const double dfb = dd.x, dgb = dd.y, ivb = sm.colbuf[cslot][ci + u].z;
-    const int ph = (R - u) & (R - 1);  // physical register of slot 0 at this step
-    if (FIRST && u == 0) {
+  for (int r = 0; r < R; ++r) out[r] = 0.0;
+  double es = 0.0;
+  const int base = R * lane;
+  for (int t0 = 0; t0 < m; t0 += T) {
+    const int tl = min(T, m - t0);
+    __syncwarp();
+    for (int q = lane; q < tl; q += 32) {
+      const double u = Ug[t0 + q] - cu;
+      sm.unif[q] = u;
+      es += u;
+    }
+    for (int q = lane; q < H + tl; q += 32) {
+      const int64_t gi = (int64_t)t0 + q;
+      sm.slide[padidx<R>(q)] = gi < s_avail ? Sg[gi] - cS : 0.0;
+    }
+    __syncwarp();
+    double w[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) P[r] = head[r];
-    } else {
-      const double e = (u == 0) ? *eprev : ecur[u - 1];
-      double in = shfl_up1(P[ph]);
-      if (u == 0) *sprev = P[ph]; else scur[u - 1] = P[ph];
-      P[ph] = l0 ? e : in;
+    for (int r = 0; r < R; ++r) w[r] = sm.slide[padidx<R>(base + r)];
+    int t = 0;
+    for (; t + R <= tl; t += R) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        double& c = P[(r + ph) & (R - 1)];
-        c = __fma_rn(dfa[r], dgb, c);
-        c = __fma_rn(dga[r], dfb, c);
+      for (int u = 0; u < R; ++u) {
+        const double uv = sm.unif[t + u];
+#pragma unroll
+        for (int r = 0; r < R; ++r) out[r] = __fma_rn(w[(r + u) & (R - 1)], uv, out[r]);
+        w[u] = sm.slide[padidx<R>(base + t + u + R)];
       }
     }
-    bool any = false;
+    for (; t < tl; ++t) {  // remainder
+      const double uv = sm.unif[t];
 #pragma unroll
-    for (int r = 0; r < R; ++r) any |= __double2hiint(P[(r + ph) & (R - 1)] * ivb) >= thr[r];
-    if (vote_any(any)) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        sm.scov[r][lane] = P[(r + ph) & (R - 1)];
-        sm.sthr[r][lane] = thr[r];
-      }
-      slow_all(sm, lane, ivb, cx.colbase + k, cx.row0, cx.excl);
-#pragma unroll
-      for (int r = 0; r < R; ++r) thr[r] = sm.sthr[r][lane];
+      for (int r = 0; r < R; ++r) out[r] = __fma_rn(sm.slide[padidx<R>(base + t + r)], uv, out[r]);
     }
+  }
+  if (esum) {
+    for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+    *esum = es;
   }
 }
 
-__device__ __forceinline__ void issue_chunk(WarpSmem& sm, const SweepCtx& cx, int lane, int c) {
-  // column data for steps [32c, 32c+32): lane copies its column (32 B)
+struct SweepCtx {
+  const double4* colg;  // global column data of this segment (col0 aligned)
+  double* E;            // global edge array of this segment (j = 0 .. ncol-2)
+  int ncol;
+  int colbase;     // concatenated column index of this segment's window 0
+  long long row0;  // row of this lane's slot 0
+  long long excl;  // self-join exclusion half-width
+  bool write_out;
+};
+
+// Data of one sweep step, prefetched one step ahead.
+struct StepIn {
+  double dfb, dgb, ivb, e, in;
+};
+
+// chunk c of the segment: column data for steps [32c, 32c+32) -> colbuf[c%3],
+// edge block c (E[32c .. 32c+31]) -> ring slot c%3
+template <int R>
+__device__ __forceinline__ void issue_chunk(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int c) {
   const double4* src = cx.colg + 32 * c + lane;
-  double4* dst = &sm.colbuf[c & 1][lane];
+  double4* dst = &sm.colbuf[c % 3][lane];
   cp16(dst, src);
   cp16(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16);
-  // edge block c: E[32c .. 32c+31] -> ring slot (c % 3)
   if (lane < 16) cp16(&sm.ering[(c % 3) * 32 + 2 * lane], cx.E + 32 * c + 2 * lane);
   cp_commit();
 }
 
-__device__ __forceinline__ void flush_block(WarpSmem& sm, const SweepCtx& cx, int lane, int b) {
+template <int R>
+__device__ __forceinline__ void flush_block(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int b) {
   const int j = 32 * b + lane;
   if (j < cx.ncol - 1) cx.E[j] = sm.ering[(b % 3) * 32 + lane];
 }
 
-__device__ void sweep_segment(WarpSmem& sm, const SweepCtx& cx, int lane, const double (&dfa)[R],
+// ring position of E[j]
+__device__ __forceinline__ int epos(int j) { return ((j >> 5) % 3) * 32 + (j & 31); }
+
+// loads a step's column data and incoming edge (E[k-1]), and shuffles the
+// diagonal that enters slot 0 (the previous step's slot R-1 value `v7`)
+__device__ __forceinline__ void prefetch(const double4* cb, const double* ep, double v7, StepIn& d) {
+  const double2 dd = *reinterpret_cast<const double2*>(cb);
+  d.dfb = dd.x;
+  d.dgb = dd.y;
+  d.ivb = cb->z;
+  d.e = *ep;
+  d.in = shfl_up1(v7);
+}
+
+// true when any slot's K high word reaches its threshold (balanced predicate tree)
+template <int R>
+__device__ __forceinline__ bool test_any(const double (&K)[R], const int (&thr)[R]) {
+  bool p[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) p[r] = __double2hiint(K[r]) >= thr[r];
+#pragma unroll
+  for (int w = 1; w < R; w <<= 1)
+#pragma unroll
+    for (int r = 0; r + w < R; r += 2 * w) p[r] = p[r] | p[r + w];
+  return p[0];
+}
+
+// exact update for the step whose K values are Kp (column col): full
+// double compare against the slot's best K; columns arrive in increasing
+// order, so ties keep the earlier (lower) column (profiles.hpp:70-77)
+template <int R, bool SELF>
+__device__ __forceinline__ void exact_update(WarpSmem<R>& sm, const SweepCtx& cx, int lane, const double (&Kp)[R],
+                                             int col, int (&thr)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const double K = Kp[r];
+    const int h = __double2hiint(K);
+    bool p = h >= thr[r];
+    if (SELF) {
+      const long long d = cx.row0 + r - col;
+      p = p && (d > cx.excl || d < -cx.excl);  // profiles.hpp:281-284
+    }
+    const double b = sm.bK[r][lane];
+    p = p && (K > b);
+    if (p) {
+      sm.bK[r][lane] = K;
+      sm.bj[r][lane] = col;
+      thr[r] = h >= 0 ? h - 1 : INT_MIN;
+    }
+  }
+}
+
+template <int R>
+struct SweepState {
+  double P[R];   // slot registers (rotating)
+  double Kp[R];  // K values of the step whose vote is pending
+  bool pending;
+  int colp;
+  StepIn nx;     // prefetched inputs of the next step
+};
+
+// One block of R steps starting at k0 (k0 % R == 0, R | 32). FIRST: block 0,
+// whose step 0 (heads) was done by the caller. GUARD: steps may run past ncol.
+// Ring/colbuf positions are resolved once per block: within a block the
+// edge positions E[k0 .. k0+R-1] are contiguous, only E[k0-1] may sit in the
+// previous ring block, and only step k0+R's column data in the next chunk.
+template <int R, bool SELF, bool FIRST, bool GUARD>
+__device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int k0, SweepState<R>& S,
+                                            const double (&dfa)[R], const double (&dga)[R], int (&thr)[R],
+                                            double* sbase, bool l0) {
+  const int n = cx.ncol;
+  const double4* ccur = &sm.colbuf[(k0 >> 5) % 3][k0 & 31];
+  const double4* cnext = &sm.colbuf[((k0 + R) >> 5) % 3][(k0 + R) & 31];
+  const int ebase = epos(k0);
+  const int eprev = (k0 + 95) % 96;  // ring position of E[k0 - 1]
+#pragma unroll
+  for (int u = FIRST ? 1 : 0; u < R; ++u) {
+    const int k = k0 + u;
+    if (GUARD && k >= n) break;
+    const int ph = (R - u) & (R - 1);  // physical register of slot 0 at this step
+    // fold in the incoming diagonal; lane 31 retires its bottom-row value (column k-1)
+    sbase[u == 0 ? eprev : ebase + u - 1] = S.P[ph];
+    S.P[ph] = l0 ? S.nx.e : S.nx.in;
+    const double dfb = S.nx.dfb, dgb = S.nx.dgb, ivb = S.nx.ivb;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double& c = S.P[(r + ph) & (R - 1)];
+      c = __fma_rn(dfa[r], dgb, c);
+      c = __fma_rn(dga[r], dfb, c);
+    }
+    if (!GUARD || k + 1 < n)
+      prefetch(u + 1 < R ? ccur + u + 1 : cnext, &sm.ering[ebase + u], S.P[(ph + R - 1) & (R - 1)], S.nx);
+    if (S.pending) exact_update<R, SELF>(sm, cx, lane, S.Kp, S.colp, thr);
+#pragma unroll
+    for (int r = 0; r < R; ++r) S.Kp[r] = S.P[(r + ph) & (R - 1)] * ivb;
+    S.pending = vote_any(test_any<R>(S.Kp, thr));
+    S.colp = cx.colbase + k;
+  }
+}
+
+// Software-pipelined sweep of one segment. Step k: slot r holds the
+// diagonal value of row (row0 + r) at column k in register P[(r - k) mod R].
+// Per step: fold in the incoming diagonal, 2 DFMA per slot, prefetch the next
+// step (column data, edge, shuffle), resolve the PREVIOUS step's vote
+// (deferred so vote/branch latency overlaps this step's math), then
+// K = cov * invn_b and the high-word test.
+template <int R, bool SELF>
+__device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, const double (&dfa)[R],
                               const double (&dga)[R], int (&thr)[R], const double (&head)[R]) {
-  double P[R];
+  static_assert(R == 8 || R == 16, "R must be 8 or 16");
   const int n = cx.ncol;
   const int nchunks = (n + 31) >> 5;
+  double* const sbase = lane == 31 ? sm.ering : sm.edummy;  // lane 31 stores into the ring
+  const bool l0 = lane == 0;
   __syncwarp();
   issue_chunk(sm, cx, lane, 0);
   if (nchunks > 1) issue_chunk(sm, cx, lane, 1); else cp_commit();
   cp_wait<1>();
   __syncwarp();
-  int flushed = 0;  // blocks [0, flushed) written back
-  // first 8-step block (contains k = 0)
-  if (n <= R) {
-    sweep_block<true, true>(sm, cx, lane, 0, P, dfa, dga, thr, head);
-  } else {
-    sweep_block<true, false>(sm, cx, lane, 0, P, dfa, dga, thr, head);
-    int k0 = R;
-    for (; k0 < n; k0 += R) {
-      if ((k0 & 31) == 0) {
-        const int c = k0 >> 5;  // chunk about to start
-        __syncwarp();
-        if (c >= 2 && cx.write_out) {
-          flush_block(sm, cx, lane, c - 2);
-          flushed = c - 1;
-        }
-        __syncwarp();
-        if (c + 1 < nchunks) issue_chunk(sm, cx, lane, c + 1); else cp_commit();
-        cp_wait<1>();
-        __syncwarp();
+  int flushed = 0;  // edge blocks [0, flushed) written back
+
+  SweepState<R> S;
+  {  // step 0: the heads
+    const double ivb = sm.colbuf[0][0].z;
+#pragma unroll
+    for (int r = 0; r < R; ++r) S.P[r] = head[r];
+    if (n > 1) prefetch(&sm.colbuf[0][1], &sm.ering[0], S.P[R - 1], S.nx);
+#pragma unroll
+    for (int r = 0; r < R; ++r) S.Kp[r] = S.P[r] * ivb;
+    S.pending = vote_any(test_any<R>(S.Kp, thr));
+    S.colp = cx.colbase;
+  }
+  auto chunk_turn = [&](int k0) {
+    // the block after this one opens chunk c: make it resident, retire edge
+    // block c-2, start loading chunk c+1 (3-deep rings keep in-use slots intact)
+    if (((k0 + R) & 31) == 0 && k0 + R < n) {
+      const int c = (k0 + R) >> 5;
+      __syncwarp();
+      if (c >= 2 && cx.write_out) {
+        flush_block(sm, cx, lane, c - 2);
+        flushed = c - 1;
       }
-      if (k0 + R <= n)
-        sweep_block<false, false>(sm, cx, lane, k0, P, dfa, dga, thr, head);
-      else
-        sweep_block<false, true>(sm, cx, lane, k0, P, dfa, dga, thr, head);
+      __syncwarp();
+      if (c + 1 < nchunks) issue_chunk(sm, cx, lane, c + 1); else cp_commit();
+      cp_wait<1>();
+      __syncwarp();
+    }
+  };
+  if (n <= R) {
+    sweep_block<R, SELF, true, true>(sm, cx, lane, 0, S, dfa, dga, thr, sbase, l0);
+  } else {
+    chunk_turn(0);
+    sweep_block<R, SELF, true, false>(sm, cx, lane, 0, S, dfa, dga, thr, sbase, l0);
+    int k0 = R;
+    for (; k0 + R <= n; k0 += R) {
+      chunk_turn(k0);
+      sweep_block<R, SELF, false, false>(sm, cx, lane, k0, S, dfa, dga, thr, sbase, l0);
+    }
+    if (k0 < n) {
+      chunk_turn(k0);
+      sweep_block<R, SELF, false, true>(sm, cx, lane, k0, S, dfa, dga, thr, sbase, l0);
     }
   }
+  if (S.pending) exact_update<R, SELF>(sm, cx, lane, S.Kp, S.colp, thr);
   cp_wait<0>();
   __syncwarp();
   if (cx.write_out) {
-    const int last = (n - 2) >> 5;  // last edge block index holding j <= n-2
+    const int last = (n - 2) >> 5;  // last edge block holding j <= n-2
     for (int b = flushed; b <= last && n >= 2; ++b) flush_block(sm, cx, lane, b);
   }
   __syncwarp();
 }
 
-__global__ void __launch_bounds__(32 * WARPS) k_join_f64(const JoinArgs a) {
+template <int R, bool SELF>
+__global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join_f64(const JoinArgs a) {
+  constexpr int H = Geo<R>::H;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpSmem* smem = reinterpret_cast<WarpSmem*>(smem_raw);
+  WarpSmem<R>* smem = reinterpret_cast<WarpSmem<R>*>(smem_raw);
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  WarpSmem& sm = smem[wl];
+  WarpSmem<R>& sm = smem[wl];
   const int gw = blockIdx.x * WARPS + wl;
   const int nw = gridDim.x * WARPS;
   double* Ew = a.edges + (int64_t)gw * a.ecap;
@@ -333,19 +395,10 @@ __global__ void __launch_bounds__(32 * WARPS) k_join_f64(const JoinArgs a) {
     const int s_beg = a.group_seg[g], s_end = a.group_seg[g + 1];
     for (int b = b0; b < b1; ++b) {
       const int64_t i0 = (int64_t)b * H;
-      double dfa[R], dga[R];
-      int thr[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const int64_t i = i0 + R * lane + r;
-        const bool in = i < a.nrows;
-        const uint8_t f = in ? a.flag_a[i] : 0;
-        dfa[r] = in ? a.dfa[i] : 0.0;
-        dga[r] = in ? a.dga[i] : 0.0;
-        sm.ivan[r][lane] = in ? a.invn_a[i] : 0.0;
-        thr[r] = (f & 1) ? INT_MIN : INT_MAX;  // valid rows (flat rows: exact slow path)
-        sm.best_c[r][lane] = -2.0;              // profiles.hpp:67
-        sm.best_j[r][lane] = -1;
+        sm.bK[r][lane] = -__longlong_as_double(0x7ff0000000000000LL);
+        sm.bj[r][lane] = -1;
       }
       const double cA = a.mua[i0];
       for (int s = s_beg; s < s_end; ++s) {
@@ -354,34 +407,35 @@ __global__ void __launch_bounds__(32 * WARPS) k_join_f64(const JoinArgs a) {
         cx.colg = a.col + sg.col0;
         cx.E = Ew + a.seg_eoff[s];
         cx.ncol = sg.ncol;
-        cx.colbase = sg.col0;
+        cx.colbase = (int)sg.col0;
         cx.write_out = (b + 1 < b1);
         cx.row0 = i0 + R * lane;
         cx.excl = a.excl;
         if (b == b0 && sg.ncol >= 2) {
           // top edge of the task: E[j] = cov(re, j + delta), j = 0 .. ncol-2
+          // (row 0 has df = dg = 0, so E[j] = cov(0, j+1) feeds it exactly)
           const int64_t re = i0 >= 1 ? i0 - 1 : 0;
           const int delta = i0 >= 1 ? 0 : 1;
           for (int q0 = delta; q0 < sg.ncol - 1 + delta; q0 += H) {
             double out[R];
             double eU;
             const double cS = a.mub[sg.col0 + q0];
-            sliding_dot(sm, a.xa + re, a.mua[re], a.xb + sg.col0 + q0, (int64_t)sg.ncol + a.m - 1 - q0, cS, a.m,
-                        lane, out, &eU);
+            sliding_dot<R>(sm, a.xa + re, a.mua[re], a.xb + sg.col0 + q0, (int64_t)sg.ncol + a.m - 1 - q0, cS,
+                           a.m, lane, out, &eU);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               const int q = q0 + R * lane + r;
               if (q < sg.ncol - 1 + delta) cx.E[q - delta] = out[r] - (a.mub[sg.col0 + q] - cS) * eU;
             }
           }
-          __syncwarp();
           __threadfence_block();
+          __syncwarp();
         }
         // left edge: cov(i, col0) for the band's rows
         double head[R];
         {
           double out[R];
-          sliding_dot(sm, a.btil + (int64_t)s * a.m, 0.0, a.xa + i0, a.na - i0, cA, a.m, lane, out, nullptr);
+          sliding_dot<R>(sm, a.btil + (int64_t)s * a.m, 0.0, a.xa + i0, a.na - i0, cA, a.m, lane, out, nullptr);
           const double e = a.ebt[s];
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -390,17 +444,34 @@ __global__ void __launch_bounds__(32 * WARPS) k_join_f64(const JoinArgs a) {
             head[r] = out[r] - (mu - cA) * e;
           }
         }
-        sweep_segment(sm, cx, lane, dfa, dga, thr, head);
+        // row data (reloaded per segment so it is not live across the heads);
+        // thresholds re-derived from the best K so far
+        double dfa[R], dga[R];
+        int thr[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int64_t i = i0 + R * lane + r;
+          const bool in = i < a.nrows;
+          const uint8_t f = in ? a.flag_a[i] : 0;
+          dfa[r] = in ? a.dfa[i] : 0.0;
+          dga[r] = in ? a.dga[i] : 0.0;
+          const double bk = sm.bK[r][lane];
+          const int h = __double2hiint(bk);
+          thr[r] = (f != 1) ? INT_MAX : (sm.bj[r][lane] < 0 || h < 0) ? INT_MIN : h - 1;
+        }
+        sweep_segment<R, SELF>(sm, cx, lane, dfa, dga, thr, head);
       }
-      // band results
+      // band results: c = clamp(K * invn_a) (profiles.hpp:331, :335)
       double* oc = a.out_c + (int64_t)g * a.nrows;
       int64_t* oj = a.out_j + (int64_t)g * a.nrows;
+      __syncwarp();
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int64_t i = i0 + R * lane + r;
         if (i < a.nrows) {
-          oc[i] = sm.best_c[r][lane];
-          oj[i] = sm.best_j[r][lane];
+          const int j = sm.bj[r][lane];
+          oc[i] = j >= 0 ? clamp_corr(sm.bK[r][lane] * a.invn_a[i]) : -2.0;
+          oj[i] = j;
         }
       }
       __syncwarp();
@@ -455,13 +526,49 @@ __global__ void k_btil(const double* __restrict__ xb, const double* __restrict__
   }
 }
 
+// flat-column table: per 1024-column block the lowest flat column, then a
+// suffix minimum over blocks; next_flat(x) = lowest flat column >= x
+constexpr int FB = 1024;
+__global__ void k_flat_bmin(const uint8_t* __restrict__ flag, int64_t ncols, int64_t* __restrict__ bmin) {
+  __shared__ unsigned long long mn;
+  if (threadIdx.x == 0) mn = ~0ull;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * FB;
+  for (int t = threadIdx.x; t < FB; t += blockDim.x) {
+    const int64_t x = base + t;
+    if (x < ncols && (flag[x] & 2)) atomicMin(&mn, (unsigned long long)x);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) bmin[blockIdx.x] = mn == ~0ull ? -1 : (int64_t)mn;
+}
+__global__ void k_flat_suffix(int64_t* __restrict__ bmin, int64_t nb) {
+  int64_t run = -1;
+  for (int64_t b = nb - 1; b >= 0; --b) {
+    if (bmin[b] >= 0) run = bmin[b];
+    bmin[b] = run;
+  }
+}
+__device__ int64_t next_flat(const uint8_t* __restrict__ flag, const int64_t* __restrict__ bsuf, int64_t ncols,
+                             int64_t x) {
+  if (x >= ncols) return -1;
+  if (x < 0) x = 0;
+  const int64_t b = x / FB, end = min(ncols, (b + 1) * FB);
+  for (int64_t t = x; t < end; ++t)
+    if (flag[t] & 2) return t;
+  return (b + 1) * FB < ncols ? bsuf[b + 1] : -1;
+}
+
+// Epilogue. Flat rows (profiles.hpp:332-336): c = 1 at the lowest admissible
+// flat column, else c = 0 at the lowest admissible column.
 __global__ void k_epilogue(const double* __restrict__ bc, const int64_t* __restrict__ bj,
                            const uint8_t* __restrict__ flag, int64_t nrows, const SegDev* __restrict__ segs, int nseg,
                            int m, const int64_t* __restrict__ s_woff, const int64_t* __restrict__ s_ooff, int nser,
-                           double* __restrict__ val, int64_t* __restrict__ idx) {
+                           const uint8_t* __restrict__ cflag, const int64_t* __restrict__ bsuf, int64_t ncols,
+                           long long excl, double* __restrict__ val, int64_t* __restrict__ idx) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nrows) return;
-  if (!(flag[i] & 1)) return;
+  const uint8_t f = flag[i];
+  if (!(f & 1)) return;
   int64_t o = i;
   if (nser > 1) {  // batched: row -> (series, window) -> packed output slot
     int lo = 0, hi = nser - 1, q = 0;
@@ -476,8 +583,24 @@ __global__ void k_epilogue(const double* __restrict__ bc, const int64_t* __restr
     }
     o = i - s_woff[q] + s_ooff[q];
   }
-  const double c = bc[i];
-  const int64_t j = bj[i];
+  double c = bc[i];
+  int64_t j = bj[i];
+  if (f & 2) {
+    const int64_t f0 = next_flat(cflag, bsuf, ncols, 0);
+    if (excl < 0) {
+      c = f0 >= 0 ? 1.0 : 0.0;
+      j = f0 >= 0 ? f0 : segs[0].col0;
+    } else {  // self-join: single segment, columns == rows
+      const int64_t fj = (f0 >= 0 && f0 < i - excl) ? f0 : next_flat(cflag, bsuf, ncols, i + excl + 1);
+      if (fj >= 0) {
+        c = 1.0;
+        j = fj;
+      } else {
+        c = 0.0;
+        j = i > excl ? 0 : (i + excl + 1 < ncols ? i + excl + 1 : -1);
+      }
+    }
+  }
   if (j < 0) {  // no admissible neighbour (profiles.hpp:149-151)
     val[o] = __longlong_as_double(0x7ff0000000000000LL);
     idx[o] = -1;
@@ -509,46 +632,77 @@ __global__ void k_epilogue(const double* __restrict__ bc, const int64_t* __restr
     }                                                                                       \
   } while (0)
 
-int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st, Error* err,
-             int* launches) {
-  if (in.precision != 0) {
-    if (err) *err = Error{kInvalidArgument, "fp32 precision mode is not built in this version"};
-    return kInvalidArgument;
-  }
+namespace {
+
+template <int R, bool SELF>
+int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st, Error* err,
+                int* launches) {
+  constexpr int H = Geo<R>::H;
   const int m = in.m;
   const int nseg = (int)in.segs.size();
   const int64_t nrows = in.rows.nwin;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem_bytes = sizeof(WarpSmem) * WARPS;
-  CUDA_TRY(cudaFuncSetAttribute(k_join_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
+  const size_t smem_bytes = sizeof(WarpSmem<R>) * WARPS;
+  auto kern = k_join_f64<R, SELF>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_join_f64, 32 * WARPS, smem_bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * WARPS, smem_bytes);
   if (occ < 1) occ = 1;
   const int nwarps = nsm * occ * WARPS;
   const int nbands = (int)((nrows + H - 1) / H);
 
-  // segment groups: start with one group; split the dictionary while the
-  // band count alone cannot fill the machine twice over
+  // Decomposition: tasks = (range of bpt bands) x (group of consecutive
+  // segments). Cost model in FP64-op units per warp: a band sweeps its
+  // group's cells (3 ops) plus one m-term head per row per segment; the first
+  // band of a task also computes the group's top edge (m terms per column).
+  // Pick (G, bpt) minimising waves * task cost; G > 1 costs a merge pass.
   int64_t total_cols = 0;
   for (const auto& s : in.segs) total_cols += s.ncol;
-  int G = 1;
-  while ((int64_t)nbands * G < 2LL * nwarps && G < nseg) G *= 2;
-  if (G > nseg) G = nseg;
-  std::vector<int> group_seg(G + 1, nseg);
-  {
+  auto split = [&](int G, std::vector<int>& gs) {
+    gs.assign(G + 1, nseg);
+    gs[0] = 0;
     int s = 0;
     int64_t acc = 0;
-    group_seg[0] = 0;
     for (int g = 1; g < G; ++g) {
       const int64_t target = total_cols * g / G;
-      while (s < nseg && acc + in.segs[s].ncol <= target) acc += in.segs[s++].ncol;
-      if (s <= group_seg[g - 1]) s = std::min(nseg, group_seg[g - 1] + 1), acc = 0;
-      group_seg[g] = s;
+      while (s < nseg - (G - g) && acc + in.segs[s].ncol <= target) acc += in.segs[s++].ncol;
+      if (s <= gs[g - 1]) acc += in.segs[s++].ncol;
+      gs[g] = s;
     }
-    group_seg[G] = nseg;
+  };
+  int G = 1, bpt = 1;
+  {
+    double best = 1e300;
+    std::vector<int> gs;
+    for (int g = 1; g <= nseg && g <= 256; g *= 2) {
+      split(g, gs);
+      int64_t cmax = 0, smax = 0;
+      for (int q = 0; q < g; ++q) {
+        int64_t c = 0;
+        for (int s = gs[q]; s < gs[q + 1]; ++s) c += in.segs[s].ncol;
+        cmax = std::max(cmax, c);
+        smax = std::max<int64_t>(smax, gs[q + 1] - gs[q]);
+      }
+      const double band = (double)H * (3.0 * cmax + (double)smax * (m + 64)) + 24.0 * cmax;
+      const double top = (double)cmax * m;
+      const int bmax = std::min(nbands, 4096);
+      for (int b = 1; b <= bmax; ++b) {
+        const int64_t nt = (int64_t)((nbands + b - 1) / b) * g;
+        const int64_t waves = (nt + nwarps - 1) / nwarps;
+        const double cost = waves * (b * band + top) + (g > 1 ? 2e3 * (double)nrows * g / nwarps : 0.0);
+        if (cost < best * 0.999) {
+          best = cost;
+          G = g;
+          bpt = b;
+        }
+        if (waves == 1) break;  // larger b only adds work per task
+      }
+    }
   }
+  std::vector<int> group_seg;
+  split(G, group_seg);
   std::vector<int> eoff(nseg);
   int64_t ecap = 0;
   for (int g = 0; g < G; ++g) {
@@ -560,14 +714,14 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     ecap = std::max(ecap, off);
   }
   ecap = (ecap + 64 + 31) & ~int64_t(31);
-  int bpt = (int)(((int64_t)nbands * G + nwarps - 1) / nwarps);
-  if (bpt < 1) bpt = 1;
   const int nbr = (nbands + bpt - 1) / bpt;
   const int ntasks = nbr * G;
   const int grid = std::max(1, std::min(nsm * occ, (ntasks + WARPS - 1) / WARPS));
   const int used_warps = grid * WARPS;
+  if (getenv("TSD_VERBOSE"))
+    fprintf(stderr, "[tsd] join R=%d rows=%lld bands=%d cols=%lld segs=%d -> G=%d bpt=%d tasks=%d warps=%d occ=%d\n", R,
+            (long long)nrows, nbands, (long long)total_cols, nseg, G, bpt, ntasks, used_warps, occ);
 
-  // device scratch
   SegDev* d_segs = (SegDev*)arena.get(sizeof(SegDev) * nseg);
   int* d_eoff = (int*)arena.get(sizeof(int) * nseg);
   int* d_gs = (int*)arena.get(sizeof(int) * (G + 1));
@@ -617,7 +771,7 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
   a.edges = d_edges;
   a.out_c = d_pc;
   a.out_j = d_pj;
-  k_join_f64<<<grid, 32 * WARPS, smem_bytes, st>>>(a);
+  kern<<<grid, 32 * WARPS, smem_bytes, st>>>(a);
   ++nl;
   if (G > 1) {
     k_merge_groups<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(d_pc, d_pj, nrows, G);
@@ -630,11 +784,42 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
   return kOk;
 }
 
+int rows_per_lane() {
+  const char* e = getenv("TSD_ROWS_PER_LANE");
+  return (e && atoi(e) == 16) ? 16 : 8;
+}
+
+}  // namespace
+
+int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st, Error* err,
+             int* launches) {
+  if (in.precision != 0) {
+    if (err) *err = Error{kInvalidArgument, "fp32 precision mode is not built in this version"};
+    return kInvalidArgument;
+  }
+  const bool self = in.excl >= 0;
+  if (rows_per_lane() == 16)
+    return self ? launch_join<16, true>(in, d_best_c, d_best_j, arena, st, err, launches)
+                : launch_join<16, false>(in, d_best_c, d_best_j, arena, st, err, launches);
+  return self ? launch_join<8, true>(in, d_best_c, d_best_j, arena, st, err, launches)
+              : launch_join<8, false>(in, d_best_c, d_best_j, arena, st, err, launches);
+}
+
 int run_epilogue(const double* d_best_c, const int64_t* d_best_j, const uint8_t* d_row_flag, int64_t nrows,
                  const SegDev* d_segs, int nseg, int m, const int64_t* d_woff, const int64_t* d_ooff, int nser,
-                 double* d_val, int64_t* d_idx, cudaStream_t st, Error* err) {
+                 const uint8_t* d_col_flag, int64_t ncols, int64_t excl, double* d_val, int64_t* d_idx, Arena& arena,
+                 cudaStream_t st, Error* err) {
+  const int64_t nb = (ncols + FB - 1) / FB;
+  int64_t* d_bsuf = (int64_t*)arena.get(sizeof(int64_t) * (nb + 1));
+  if (!d_bsuf) {
+    if (err) *err = Error{kCudaError, "device allocation failed for the epilogue"};
+    return kCudaError;
+  }
+  k_flat_bmin<<<(unsigned)nb, 256, 0, st>>>(d_col_flag, ncols, d_bsuf);
+  k_flat_suffix<<<1, 1, 0, st>>>(d_bsuf, nb);
   k_epilogue<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(d_best_c, d_best_j, d_row_flag, nrows, d_segs, nseg, m,
-                                                               d_woff, d_ooff, nser, d_val, d_idx);
+                                                               d_woff, d_ooff, nser, d_col_flag, d_bsuf, ncols,
+                                                               (long long)excl, d_val, d_idx);
   CUDA_TRY(cudaGetLastError());
   return kOk;
 }

@@ -114,8 +114,11 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
 // admissible neighbour (profiles.hpp:149-151), row compaction for batched
 // queries: series q's valid windows start at row d_woff[q] and are written
 // from output slot d_ooff[q] on (nser == 1: identity).
+// Flat rows (invn_a == 0) are resolved here from the column flags
+// (d_col_flag over ncols concatenated columns; excl >= 0 for the self-join).
 int run_epilogue(const double* d_best_c, const int64_t* d_best_j, const uint8_t* d_row_flag, int64_t nrows,
                  const SegDev* d_segs, int nseg, int m, const int64_t* d_woff, const int64_t* d_ooff, int nser,
-                 double* d_val, int64_t* d_idx, cudaStream_t st, Error* err);
+                 const uint8_t* d_col_flag, int64_t ncols, int64_t excl, double* d_val, int64_t* d_idx, Arena& arena,
+                 cudaStream_t st, Error* err);
 
 }  // namespace tsd

@@ -41,7 +41,7 @@ ov, oi = O.dict_join(q, list(segs), [512 * s for s in range(8)], 100)
 cmp("C1 dict join", P.values, P.indices, ov, oi)
 
 # timing: C3-sized-ish (2^20 x 32 x 2048, m=200) and C4 prefix
-for (nq, nseg, L, m) in [(1 << 20, 32, 2048, 200), (1 << 22, 256, 1024, 512)]:
+for (nq, nseg, L, m) in [(1 << 20, 32, 2048, 200), (1 << 22, 256, 1024, 512)][:int(os.environ.get('NTIME','2'))]:
     q = synth.walk(4, nq); segs = synth.walks(5, nseg, L)
     D = t.Dictionary([t.Segment(L * s, segs[s]) for s in range(nseg)], m=m, source_length=nseg * L)
     plan = t.DictPlan(D, m)
