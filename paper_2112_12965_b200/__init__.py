@@ -21,7 +21,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtsdict_cuda.so")
+LIB_PATH = os.environ.get("TSD_LIB") or os.path.join(_HERE, "libtsdict_cuda.so")
 
 __all__ = [
     "errc", "TsdictError", "TimeSeries", "SubseqStats", "MatrixProfile", "Segment", "Dictionary",

@@ -89,8 +89,8 @@ struct __align__(16) WarpSmem {
   double4 colbuf[3][32];
   double ering[96];
   double edummy[96];  // lanes 0..30 store here so lane 31's edge store needs no branch
-  double bK[R][32];   // best K per slot (exact compare in the update path)
-  int bj[R][32];      // its concatenated column
+  double bK[R][32];  // best K = cov * invn_b per slot (row factor invn_a left out)
+  int bj[R][32];     // its concatenated column
   double slide[Geo<R>::SLIDE];
   double unif[T];
 };
@@ -145,17 +145,20 @@ __device__ void sliding_dot(WarpSmem<R>& sm, const double* __restrict__ Ug, doub
       sm.slide[padidx<R>(q)] = gi < s_avail ? Sg[gi] - cS : 0.0;
     }
     __syncwarp();
+    // padidx(base + t + j) = padidx(base + t) + j + j / R for t % R == 0
+    const double* sp = &sm.slide[padidx<R>(base)];
+    const double* up = sm.unif;
     double w[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) w[r] = sm.slide[padidx<R>(base + r)];
+    for (int r = 0; r < R; ++r) w[r] = sp[r];
     int t = 0;
-    for (; t + R <= tl; t += R) {
+    for (; t + R <= tl; t += R, sp += R + 1, up += R) {
 #pragma unroll
       for (int u = 0; u < R; ++u) {
-        const double uv = sm.unif[t + u];
+        const double uv = up[u];
 #pragma unroll
         for (int r = 0; r < R; ++r) out[r] = __fma_rn(w[(r + u) & (R - 1)], uv, out[r]);
-        w[u] = sm.slide[padidx<R>(base + t + u + R)];
+        w[u] = sp[u + R + 1];  // sample base + t + u + R
       }
     }
     for (; t < tl; ++t) {  // remainder
@@ -180,11 +183,6 @@ struct SweepCtx {
   bool write_out;
 };
 
-// Data of one sweep step, prefetched one step ahead.
-struct StepIn {
-  double dfb, dgb, ivb, e, in;
-};
-
 // chunk c of the segment: column data for steps [32c, 32c+32) -> colbuf[c%3],
 // edge block c (E[32c .. 32c+31]) -> ring slot c%3
 template <int R>
@@ -203,115 +201,114 @@ __device__ __forceinline__ void flush_block(WarpSmem<R>& sm, const SweepCtx& cx,
   if (j < cx.ncol - 1) cx.E[j] = sm.ering[(b % 3) * 32 + lane];
 }
 
-// ring position of E[j]
-__device__ __forceinline__ int epos(int j) { return ((j >> 5) % 3) * 32 + (j & 31); }
+// Per-slot test threshold for a block: the high word of bestK * min_norm_b
+// over the block's columns, minus one. cov*invn_b > bestK implies
+// cov > bestK * norm_b >= bestK * min_norm_b, so hi(cov) >= thr whenever the
+// cell can improve the row (bestK > 0); bestK <= 0 (no positive candidate
+// yet) passes everything, inactive rows carry bestK = +inf and never pass.
+__device__ __forceinline__ int block_thr(double bK, double mnorm) {
+  const int h = __double2hiint(bK * mnorm);
+  return h > 0 ? h - 1 : INT_MIN;
+}
 
-// loads a step's column data and incoming edge (E[k-1]), and shuffles the
-// diagonal that enters slot 0 (the previous step's slot R-1 value `v7`)
+struct StepIn {
+  double dfb, dgb, e, in;
+};
+
 __device__ __forceinline__ void prefetch(const double4* cb, const double* ep, double v7, StepIn& d) {
   const double2 dd = *reinterpret_cast<const double2*>(cb);
   d.dfb = dd.x;
   d.dgb = dd.y;
-  d.ivb = cb->z;
   d.e = *ep;
   d.in = shfl_up1(v7);
 }
 
-// true when any slot's K high word reaches its threshold (balanced predicate tree)
 template <int R>
-__device__ __forceinline__ bool test_any(const double (&K)[R], const int (&thr)[R]) {
-  bool p[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) p[r] = __double2hiint(K[r]) >= thr[r];
-#pragma unroll
-  for (int w = 1; w < R; w <<= 1)
-#pragma unroll
-    for (int r = 0; r + w < R; r += 2 * w) p[r] = p[r] | p[r + w];
-  return p[0];
-}
+struct SweepState {
+  double P[R];  // slot registers: step k, slot r at P[(r - k) mod R]
+  int thr[R];   // high-word test thresholds of the current block
+  StepIn nx;    // prefetched inputs of the next step
+};
 
-// exact update for the step whose K values are Kp (column col): full
-// double compare against the slot's best K; columns arrive in increasing
-// order, so ties keep the earlier (lower) column (profiles.hpp:70-77)
+// Exact update (taken by the warp when some lane's coarse test passed):
+// K = cov * invn_b for every slot, full double compare with the slot's best
+// K; columns arrive in increasing order, so ties keep the earlier (lower)
+// column (profiles.hpp:70-77).
 template <int R, bool SELF>
-__device__ __forceinline__ void exact_update(WarpSmem<R>& sm, const SweepCtx& cx, int lane, const double (&Kp)[R],
-                                             int col, int (&thr)[R]) {
+__device__ __forceinline__ void exact_step(WarpSmem<R>& sm, int lane, const SweepState<R>& S, int ph, double ivb,
+                                           double mnorm, int col, long long row0, long long excl, int (&thr)[R]) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const double K = Kp[r];
-    const int h = __double2hiint(K);
-    bool p = h >= thr[r];
+    const double cov = S.P[(r + ph) & (R - 1)];
+    bool ok = __double2hiint(cov) >= thr[r];
     if (SELF) {
-      const long long d = cx.row0 + r - col;
-      p = p && (d > cx.excl || d < -cx.excl);  // profiles.hpp:281-284
+      const long long d = row0 + r - col;
+      ok = ok && (d > excl || d < -excl);  // profiles.hpp:281-284
     }
-    const double b = sm.bK[r][lane];
-    p = p && (K > b);
-    if (p) {
+    const double K = cov * ivb;
+    if (ok && K > sm.bK[r][lane]) {
       sm.bK[r][lane] = K;
       sm.bj[r][lane] = col;
-      thr[r] = h >= 0 ? h - 1 : INT_MIN;
+      thr[r] = block_thr(K, mnorm);
     }
   }
 }
 
-template <int R>
-struct SweepState {
-  double P[R];   // slot registers (rotating)
-  double Kp[R];  // K values of the step whose vote is pending
-  bool pending;
-  int colp;
-  StepIn nx;     // prefetched inputs of the next step
-};
-
 // One block of R steps starting at k0 (k0 % R == 0, R | 32). FIRST: block 0,
-// whose step 0 (heads) was done by the caller. GUARD: steps may run past ncol.
-// Ring/colbuf positions are resolved once per block: within a block the
-// edge positions E[k0 .. k0+R-1] are contiguous, only E[k0-1] may sit in the
-// previous ring block, and only step k0+R's column data in the next chunk.
+// whose step 0 (heads, already in P) only needs its test. GUARD: steps may
+// run past ncol. Ring/colbuf positions are resolved once per block: E[k0 ..
+// k0+R-1] are contiguous, only E[k0-1] may sit in the previous ring block,
+// and only step k0+R's column data in the next chunk.
 template <int R, bool SELF, bool FIRST, bool GUARD>
 __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int k0, SweepState<R>& S,
-                                            const double (&dfa)[R], const double (&dga)[R], int (&thr)[R],
-                                            double* sbase, bool l0) {
+                                            const double (&dfa)[R], const double (&dga)[R], double* sbase, bool l0) {
   const int n = cx.ncol;
   const double4* ccur = &sm.colbuf[(k0 >> 5) % 3][k0 & 31];
   const double4* cnext = &sm.colbuf[((k0 + R) >> 5) % 3][(k0 + R) & 31];
-  const int ebase = epos(k0);
-  const int eprev = (k0 + 95) % 96;  // ring position of E[k0 - 1]
+  const int ebase = k0 % 96;                       // ring position of E[k0]
+  double* const st_prev = sbase + (k0 + 95) % 96;  // E[k0-1]
+  double* const st_cur = sbase + ebase;
+  const double mnorm = ccur->w;  // min norm_b over this block's columns
 #pragma unroll
-  for (int u = FIRST ? 1 : 0; u < R; ++u) {
+  for (int r = 0; r < R; ++r) S.thr[r] = block_thr(sm.bK[r][lane], mnorm);
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
     const int k = k0 + u;
     if (GUARD && k >= n) break;
     const int ph = (R - u) & (R - 1);  // physical register of slot 0 at this step
-    // fold in the incoming diagonal; lane 31 retires its bottom-row value (column k-1)
-    sbase[u == 0 ? eprev : ebase + u - 1] = S.P[ph];
-    S.P[ph] = l0 ? S.nx.e : S.nx.in;
-    const double dfb = S.nx.dfb, dgb = S.nx.dgb, ivb = S.nx.ivb;
+    if (!(FIRST && u == 0)) {
+      // fold in the incoming diagonal; lane 31 retires its bottom-row value (column k-1)
+      (u == 0 ? st_prev : st_cur + u - 1)[0] = S.P[ph];
+      S.P[ph] = l0 ? S.nx.e : S.nx.in;
+      const double dfb = S.nx.dfb, dgb = S.nx.dgb;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      double& c = S.P[(r + ph) & (R - 1)];
-      c = __fma_rn(dfa[r], dgb, c);
-      c = __fma_rn(dga[r], dfb, c);
+      for (int r = 0; r < R; ++r) {
+        double& c = S.P[(r + ph) & (R - 1)];
+        c = __fma_rn(dfa[r], dgb, c);
+        c = __fma_rn(dga[r], dfb, c);
+      }
     }
     if (!GUARD || k + 1 < n)
       prefetch(u + 1 < R ? ccur + u + 1 : cnext, &sm.ering[ebase + u], S.P[(ph + R - 1) & (R - 1)], S.nx);
-    if (S.pending) exact_update<R, SELF>(sm, cx, lane, S.Kp, S.colp, thr);
+    bool p[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) S.Kp[r] = S.P[(r + ph) & (R - 1)] * ivb;
-    S.pending = vote_any(test_any<R>(S.Kp, thr));
-    S.colp = cx.colbase + k;
+    for (int r = 0; r < R; ++r) p[r] = __double2hiint(S.P[(r + ph) & (R - 1)]) >= S.thr[r];
+#pragma unroll
+    for (int w = 1; w < R; w <<= 1)
+#pragma unroll
+      for (int r = 0; r + w < R; r += 2 * w) p[r] = p[r] | p[r + w];
+    if (__builtin_expect(vote_any(p[0]), 0))
+      exact_step<R, SELF>(sm, lane, S, ph, (ccur + u)->z, mnorm, cx.colbase + k, cx.row0, cx.excl, S.thr);
   }
 }
 
-// Software-pipelined sweep of one segment. Step k: slot r holds the
-// diagonal value of row (row0 + r) at column k in register P[(r - k) mod R].
-// Per step: fold in the incoming diagonal, 2 DFMA per slot, prefetch the next
-// step (column data, edge, shuffle), resolve the PREVIOUS step's vote
-// (deferred so vote/branch latency overlaps this step's math), then
-// K = cov * invn_b and the high-word test.
+// Software-pipelined sweep of one segment. Per step: fold in the incoming
+// diagonal, 2 DFMA per slot, prefetch the next step's column data / edge /
+// shuffle, then the high-word test of every slot against its block threshold
+// (no per-cell multiply) and one warp vote.
 template <int R, bool SELF>
 __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, const double (&dfa)[R],
-                              const double (&dga)[R], int (&thr)[R], const double (&head)[R]) {
+                              const double (&dga)[R], SweepState<R>& S) {
   static_assert(R == 8 || R == 16, "R must be 8 or 16");
   const int n = cx.ncol;
   const int nchunks = (n + 31) >> 5;
@@ -323,18 +320,7 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   cp_wait<1>();
   __syncwarp();
   int flushed = 0;  // edge blocks [0, flushed) written back
-
-  SweepState<R> S;
-  {  // step 0: the heads
-    const double ivb = sm.colbuf[0][0].z;
-#pragma unroll
-    for (int r = 0; r < R; ++r) S.P[r] = head[r];
-    if (n > 1) prefetch(&sm.colbuf[0][1], &sm.ering[0], S.P[R - 1], S.nx);
-#pragma unroll
-    for (int r = 0; r < R; ++r) S.Kp[r] = S.P[r] * ivb;
-    S.pending = vote_any(test_any<R>(S.Kp, thr));
-    S.colp = cx.colbase;
-  }
+  if (n > 1) prefetch(&sm.colbuf[0][1], &sm.ering[0], S.P[R - 1], S.nx);
   auto chunk_turn = [&](int k0) {
     // the block after this one opens chunk c: make it resident, retire edge
     // block c-2, start loading chunk c+1 (3-deep rings keep in-use slots intact)
@@ -352,21 +338,20 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
     }
   };
   if (n <= R) {
-    sweep_block<R, SELF, true, true>(sm, cx, lane, 0, S, dfa, dga, thr, sbase, l0);
+    sweep_block<R, SELF, true, true>(sm, cx, lane, 0, S, dfa, dga, sbase, l0);
   } else {
     chunk_turn(0);
-    sweep_block<R, SELF, true, false>(sm, cx, lane, 0, S, dfa, dga, thr, sbase, l0);
+    sweep_block<R, SELF, true, false>(sm, cx, lane, 0, S, dfa, dga, sbase, l0);
     int k0 = R;
     for (; k0 + R <= n; k0 += R) {
       chunk_turn(k0);
-      sweep_block<R, SELF, false, false>(sm, cx, lane, k0, S, dfa, dga, thr, sbase, l0);
+      sweep_block<R, SELF, false, false>(sm, cx, lane, k0, S, dfa, dga, sbase, l0);
     }
     if (k0 < n) {
       chunk_turn(k0);
-      sweep_block<R, SELF, false, true>(sm, cx, lane, k0, S, dfa, dga, thr, sbase, l0);
+      sweep_block<R, SELF, false, true>(sm, cx, lane, k0, S, dfa, dga, sbase, l0);
     }
   }
-  if (S.pending) exact_update<R, SELF>(sm, cx, lane, S.Kp, S.colp, thr);
   cp_wait<0>();
   __syncwarp();
   if (cx.write_out) {
@@ -387,6 +372,7 @@ __global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join
   const int nw = gridDim.x * WARPS;
   double* Ew = a.edges + (int64_t)gw * a.ecap;
   const int bpt = a.bands_per_task;
+  const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 
   for (int task = gw; task < a.ntasks; task += nw) {
     const int g = task % a.ngroups;
@@ -397,7 +383,9 @@ __global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join
       const int64_t i0 = (int64_t)b * H;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        sm.bK[r][lane] = -__longlong_as_double(0x7ff0000000000000LL);
+        const int64_t i = i0 + R * lane + r;
+        const uint8_t f = i < a.nrows ? a.flag_a[i] : 0;
+        sm.bK[r][lane] = f == 1 ? -kInf : kInf;  // valid non-flat rows take part; +inf never passes
         sm.bj[r][lane] = -1;
       }
       const double cA = a.mua[i0];
@@ -431,9 +419,8 @@ __global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join
           __threadfence_block();
           __syncwarp();
         }
-        // left edge: cov(i, col0) for the band's rows
-        double head[R];
-        {
+        SweepState<R> S;
+        {  // left edge: cov(i, col0) for the band's rows
           double out[R];
           sliding_dot<R>(sm, a.btil + (int64_t)s * a.m, 0.0, a.xa + i0, a.na - i0, cA, a.m, lane, out, nullptr);
           const double e = a.ebt[s];
@@ -441,25 +428,19 @@ __global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join
           for (int r = 0; r < R; ++r) {
             const int64_t i = i0 + R * lane + r;
             const double mu = i < a.nrows ? a.mua[i] : cA;
-            head[r] = out[r] - (mu - cA) * e;
+            S.P[r] = out[r] - (mu - cA) * e;
           }
         }
-        // row data (reloaded per segment so it is not live across the heads);
-        // thresholds re-derived from the best K so far
+        // row data (reloaded per segment so it is not live across the heads)
         double dfa[R], dga[R];
-        int thr[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int64_t i = i0 + R * lane + r;
           const bool in = i < a.nrows;
-          const uint8_t f = in ? a.flag_a[i] : 0;
           dfa[r] = in ? a.dfa[i] : 0.0;
           dga[r] = in ? a.dga[i] : 0.0;
-          const double bk = sm.bK[r][lane];
-          const int h = __double2hiint(bk);
-          thr[r] = (f != 1) ? INT_MAX : (sm.bj[r][lane] < 0 || h < 0) ? INT_MIN : h - 1;
         }
-        sweep_segment<R, SELF>(sm, cx, lane, dfa, dga, thr, head);
+        sweep_segment<R, SELF>(sm, cx, lane, dfa, dga, S);
       }
       // band results: c = clamp(K * invn_a) (profiles.hpp:331, :335)
       double* oc = a.out_c + (int64_t)g * a.nrows;
@@ -497,11 +478,20 @@ __global__ void k_merge_groups(double* __restrict__ c, int64_t* __restrict__ j, 
   j[i] = bj;
 }
 
+// column data {df, dg, invn, min norm over the next R columns} (norm = 1/invn,
+// +inf for flat / straddling windows); the sweep reads .w at block starts
 __global__ void k_pack_cols(const double* __restrict__ df, const double* __restrict__ dg,
-                            const double* __restrict__ invn, int64_t n, double4* __restrict__ col) {
+                            const double* __restrict__ invn, int64_t n, int R, double4* __restrict__ col) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n + 64) return;
-  col[i] = i < n ? make_double4(df[i], dg[i], invn[i], 0.0) : make_double4(0, 0, 0, 0);
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double mn = inf;
+  for (int q = 0; q < R; ++q) {
+    const int64_t j = i + q;
+    const double iv = j < n ? invn[j] : 0.0;
+    if (iv > 0.0) mn = fmin(mn, 1.0 / iv);
+  }
+  col[i] = i < n ? make_double4(df[i], dg[i], invn[i], mn) : make_double4(0, 0, 0, mn);
 }
 
 __global__ void k_btil(const double* __restrict__ xb, const double* __restrict__ mub, const SegDev* __restrict__ segs,
@@ -740,7 +730,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   CUDA_TRY(cudaMemcpyAsync(d_gs, group_seg.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice, st));
   int nl = 0;
   k_pack_cols<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(in.cols.df, in.cols.dg, in.cols.invn,
-                                                                          in.cols.nwin, d_col);
+                                                                          in.cols.nwin, R, d_col);
   ++nl;
   k_btil<<<nseg, 128, 0, st>>>(in.xb, in.cols.mu, d_segs, m, d_btil, d_ebt);
   ++nl;
