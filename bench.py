@@ -1,0 +1,322 @@
+"""bench.py -- BASELINE metric on the B200: AB-join distance cells/s (GCell/s)
+and % of the FP64 roofline, next to the reference CPU join.
+
+Workload (BASELINE.json configs[3], "C4"): a 2^24-sample random-walk query
+(seed 4) joined against a dictionary of 256 random-walk segments x 1024
+samples (seed 5), m = 512, FP64 -- the config the north-star target is quoted
+on. One step = one full dictionary join of the query: window statistics +
+the join kernel + epilogue, inputs resident in HBM. Inputs are seeded
+synthetic data with the BASELINE shapes (no dataset needed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+    python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+
+N > 1: weak scaling -- every rank joins its own C4 query (seed 4 + rank)
+against the same dictionary; no collective on the data path (rows are
+independent). Timing: CUDA events on the launching stream,
+barrier + synchronize on both sides, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+Q_LEN = 1 << 24
+N_SEG = 256
+SEG_LEN = 1024
+M = 512
+Q_SEED, D_SEED = 4, 5
+FLOPS_PER_CELL = 6  # profiles.hpp:330-331: 2 mul + 2 add (update) + 2 mul (normalise)
+CPU_SAMPLE_WINDOWS = 1 << 15  # bounded CPU-baseline sample (query windows)
+
+
+def cells_per_step(q_len=Q_LEN):
+    return (q_len - M + 1) * N_SEG * (SEG_LEN - M + 1)
+
+
+def workload_config():
+    return {"workload": "C4: FP64 dictionary AB-join, random-walk query 2^24 (seed 4) vs 256 random-walk segments "
+                        "x 1024 (seed 5), m=512, straddling windows masked",
+            "query_len": Q_LEN, "segments": N_SEG, "segment_len": SEG_LEN, "m": M,
+            "cells_per_step": cells_per_step(),
+            "l2": "query (128 MiB) + window stats exceed the 126 MB L2; L2 flushed with a 256 MiB write between steps"}
+
+
+# ---------------------------------------------------------------- sharding helpers (tests/_shard_worker.py)
+def shard_rows(nrows, rank, world):
+    """contiguous query-window range [lo, hi) of `rank`; its samples are
+    [lo, hi + m - 1) (m-1 halo), so shards need no exchange"""
+    per = (nrows + world - 1) // world
+    lo = min(nrows, rank * per)
+    return lo, min(nrows, lo + per)
+
+
+def gather_rows(val, idx, rank, world):
+    """gather per-rank profile slices to rank 0 (list of (val, idx) in rank order)"""
+    import torch.distributed as dist
+    obj = [None] * world
+    dist.all_gather_object(obj, (np.asarray(val), np.asarray(idx)))
+    return obj if rank == 0 else None
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region"""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and "Active" in r[3 + k]
+                          and "Not" not in r[3 + k]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- inputs
+def make_dictionary():
+    from paper_2112_12965_b200 import synth
+    import paper_2112_12965_b200 as tsd
+    segs = synth.walks(D_SEED, N_SEG, SEG_LEN)
+    return tsd.Dictionary([tsd.Segment(SEG_LEN * s, segs[s]) for s in range(N_SEG)], m=M,
+                          source_length=N_SEG * SEG_LEN), segs
+
+
+def make_query(seed):
+    from paper_2112_12965_b200 import synth
+    return synth.walk(seed, Q_LEN)
+
+
+# ---------------------------------------------------------------- CPU baseline (reference)
+def cpu_reference_gcells(q, segs, threads, windows=CPU_SAMPLE_WINDOWS):
+    """the unmodified reference join_dictionary (oracle/_ref) on the first
+    `windows` query windows, all host threads; falls back to the plain-C port
+    (single thread) when the reference build is absent"""
+    from oracle import py_oracle as O
+    sub = q[: windows + M - 1]
+    t0 = time.perf_counter()
+    if O.ref_available():
+        O.ref_join_dictionary(sub, list(segs), [SEG_LEN * s for s in range(N_SEG)], M, threads=threads)
+        kind, cores = "reference", threads
+    else:
+        O.dict_join(sub, list(segs), [SEG_LEN * s for s in range(N_SEG)], M)
+        kind, cores = "port", 1
+    dt = time.perf_counter() - t0
+    cells = windows * N_SEG * (SEG_LEN - M + 1)
+    return {"value": cells / dt / 1e9, "unit": "GCell/s", "cores": cores, "kind": kind,
+            "sample": f"first {windows} query windows of C4 x all 256 segments ({cells:.3e} cells, {dt:.1f} s)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    _, segs = make_dictionary()
+    q = make_query(Q_SEED)
+    threads = os.cpu_count() or 1
+    vals = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_reference_gcells(q, segs, threads, windows=args.ref_windows)
+        if s >= args.warmup:
+            vals.append(r["value"])
+    v = statistics.median(vals)
+    cb = dict(r, value=v)
+    line = {"impl": "reference", "metric": "AB-join distance cells/sec", "value": v, "unit": "GCell/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cells_per_step() / (v * 1e9) * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded random walks, BASELINE C4 shapes)",
+            "config": dict(workload_config(), note="each step times the reference on a bounded sample of the "
+                                                  "workload; ms_per_step extrapolates to the full step"),
+            "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "GCell/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_gpu(args):
+    import torch
+    import paper_2112_12965_b200 as tsd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    D, segs = make_dictionary()
+    q = make_query(Q_SEED + rank)
+    nrows = Q_LEN - M + 1
+    plan = tsd.DictPlan(D, M)
+    d_q = torch.from_numpy(q).to(dev)
+    d_val = torch.empty(nrows, dtype=torch.float64, device=dev)
+    d_idx = torch.empty(nrows, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan.join_device(d_q.data_ptr(), [Q_LEN], d_val.data_ptr(), d_idx.data_ptr(), stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    launches = 0
+    join_ms = []
+    elapsed_ms = 0.0
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush between steps (not timed)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            e1.synchronize()
+            elapsed_ms += e0.elapsed_time(e1)
+            s_ms, j_ms, nl = plan.last_timing()
+            join_ms.append(j_ms)
+            launches += nl
+        torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    total_cells = cells_per_step() * world * args.steps
+    value = total_cells / (elapsed_ms * 1e-3) / 1e9
+
+    # end to end through the reference-facing C ABI (host buffers, pinned)
+    h_q = torch.from_numpy(q).pin_memory()
+    h_val = torch.empty(nrows, dtype=torch.float64).pin_memory()
+    h_idx = torch.empty(nrows, dtype=torch.int64).pin_memory()
+    seg_all = np.ascontiguousarray(np.concatenate(list(segs)))
+    lib = tsd.load_library()
+    import ctypes
+    lens = np.full(N_SEG, SEG_LEN, dtype=np.uintp)
+    starts = np.arange(N_SEG, dtype=np.uintp) * SEG_LEN
+    f64p, i64p, szp = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_size_t)
+
+    def e2e_call():
+        rc = lib.tsd_dict_join(ctypes.cast(h_q.data_ptr(), f64p), Q_LEN, seg_all.ctypes.data_as(f64p),
+                               lens.ctypes.data_as(szp), starts.ctypes.data_as(szp), N_SEG, M, 0,
+                               ctypes.cast(h_val.data_ptr(), f64p), ctypes.cast(h_idx.data_ptr(), i64p))
+        if rc:
+            raise RuntimeError(lib.tsd_last_error().decode())
+
+    e2e_call()  # warm (thread context, arena)
+    e2e_steps = max(1, min(args.steps, 3))
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_call()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = cells_per_step() * world / e2e_s / 1e9
+    # sanity: the e2e result equals the device-resident result
+    same = bool(torch.equal(h_idx, d_idx.cpu())) and bool(torch.equal(h_val, d_val.cpu()))
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return 0
+    peak = tsd.measure_peak("fp64", seconds=2.0)
+    jms = statistics.median(join_ms)
+    achieved = FLOPS_PER_CELL * cells_per_step() / (jms * 1e-3)
+    roofline = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": args.traffic,
+                "kernel": "k_join_f64 (+ its edge/merge helpers)", "achieved_def":
+                    "6 FP64 flops per valid cell (profiles.hpp:330-331) x cells per launch / median join time "
+                    "(CUDA events on the launching stream)",
+                "peak_def": "DFMA throughput measured live by tsd_measure_peak (2 s sustained, this GPU); "
+                            "MEASURED_PEAKS.json has no FP64 entry"}
+    cpu = cpu_reference_gcells(q, segs, os.cpu_count() or 1) if world == 1 or rank == 0 else None
+    line = {"metric": "AB-join distance cells/sec", "value": value, "unit": "GCell/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded random walks with the BASELINE C4 shapes)", "config": workload_config(),
+            "parallelism": f"weak x{world}: one C4 query per GPU, shared dictionary, no data-path collective",
+            "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "GCell/s", "h2d_bytes_per_step": int(Q_LEN * 8 + seg_all.nbytes),
+                    "d2h_bytes_per_step": int(nrows * 16), "api": "tsd_dict_join (host buffers, pinned)",
+                    "matches_device_path": same},
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "join_ms_median": jms, "fraction_of_fp64_peak_cells": (cells_per_step() / (jms * 1e-3)) /
+                                                                    (peak / FLOPS_PER_CELL)}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--ref-windows", type=int, default=CPU_SAMPLE_WINDOWS)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per join launch from an ncu capture (reported as roofline.traffic)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    return run_reference(args) if args.impl == "reference" else run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -214,3 +214,26 @@ def ref_sine(n, period, amp=1.0):
     o = np.empty(n)
     ref().tsdr_sine(n, period, amp, _p(o, _f64p))
     return o
+
+
+def ref_learn_dictionary(t, m, space_saving, threads=0):
+    """the reference's greedy learn_dictionary (dictionary.hpp:259-328);
+    returns (segments, starts, e_max)"""
+    t = _f(t)
+    n = t.size
+    st = np.zeros(n, dtype=np.uintp)
+    ln = np.zeros(n, dtype=np.uintp)
+    vals = np.zeros(n)
+    ns = ctypes.c_size_t()
+    em = ctypes.c_double()
+    r = ref()
+    r.tsdr_learn_dictionary.argtypes = [_f64p, _sz, _sz, ctypes.c_double, ctypes.c_uint, _szp, _szp, _f64p,
+                                        ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_double)]
+    _chk(r.tsdr_learn_dictionary(_p(t, _f64p), n, m, space_saving, threads, _p(st, _szp), _p(ln, _szp),
+                                 _p(vals, _f64p), ctypes.byref(ns), ctypes.byref(em)))
+    segs, starts, off = [], [], 0
+    for s in range(ns.value):
+        segs.append(vals[off:off + ln[s]].copy())
+        starts.append(int(st[s]))
+        off += int(ln[s])
+    return segs, starts, em.value

@@ -105,6 +105,28 @@ int tsdr_compute_e_max(const double* t, size_t n, const double* seg_vals, const 
   });
 }
 
+// learn_dictionary (dictionary.hpp:259-328) with a space-saving stop rule;
+// writes the merged segments (starts, lengths, packed values; capacity n
+// each) and returns the segment count through *nseg and e_max through *e_max.
+int tsdr_learn_dictionary(const double* t, size_t n, size_t m, double space_saving, unsigned threads,
+                          size_t* seg_start, size_t* seg_len, double* seg_vals, size_t* nseg, double* e_max) {
+  return guarded([&] {
+    tsdict::LearnConfig cfg;
+    cfg.m = m;
+    cfg.space_saving_target = space_saving;
+    const tsdict::Dictionary D = tsdict::learn_dictionary(ts(t, n), cfg, threads);
+    size_t off = 0;
+    for (size_t s = 0; s < D.segments.size(); ++s) {
+      seg_start[s] = D.segments[s].start;
+      seg_len[s] = D.segments[s].length();
+      std::memcpy(seg_vals + off, D.segments[s].values.data(), seg_len[s] * sizeof(double));
+      off += seg_len[s];
+    }
+    *nseg = D.segments.size();
+    *e_max = D.e_max.value_or(-1.0);
+  });
+}
+
 // tests/oracles.hpp long-double brute force
 int tsdr_ab_join_brute(const double* a, size_t na, const double* b, size_t nb, size_t m, double* val,
                        int64_t* idx) {

@@ -371,14 +371,13 @@ int tsd_dict_join_batched(const double* q_vals, const size_t* q_len, size_t nser
   for (size_t k = 0; k < nseries; ++k)
     if (m > q_len[k]) return fail(kWindowTooLarge, "window length exceeds series length");  // :158
   if (precision != TSD_FP64 && precision != TSD_FP32) return fail(kInvalidArgument, "unknown precision");
-  tsd_dict_plan* p = nullptr;
-  int rc = tsd_dict_plan_create(seg_vals, seg_len, seg_start, nseg, m, precision, &p);
-  if (rc) return rc;
-  rc = plan_join_host(p, q_vals, q_len, nseries, val, idx);
-  std::string keep = t_err;
-  tsd_dict_plan_destroy(p);
-  t_err = keep;
-  return rc;
+  // one cached plan per host thread: its device arenas are reused across
+  // calls, so repeated host-API joins do not pay cudaMalloc
+  thread_local tsd_dict_plan tp;
+  tp.dict_arena.reset();
+  tp.work_arena.reset();
+  if (int rc = plan_build(&tp, seg_vals, seg_len, seg_start, nseg, m, precision)) return rc;
+  return plan_join_host(&tp, q_vals, q_len, nseries, val, idx);
 }
 
 int tsd_compute_e_max(const double* t, size_t n, size_t source_length, const double* seg_vals, const size_t* seg_len,

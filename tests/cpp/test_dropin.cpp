@@ -1,0 +1,190 @@
+// test_dropin.cpp -- the C++ drop-in headers (include/tsdict/*.hpp) used the
+// way the reference's own GoogleTest suites use the reference headers
+// (tests/test_profiles.cpp, test_dict_join.cpp, test_series.cpp). Results
+// are checked against the oracle (oracle/tsd_oracle.h). One [PASS]/[FAIL]
+// line per case; exit status = number of failures. Needs a GPU.
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "tsd_oracle.h"
+#include "tsdict/tsdict.hpp"
+
+extern "C" {
+void* tsd_rng_new(uint64_t seed);
+void tsd_rng_free(void* h);
+void tsd_rng_walk(void* h, size_t n, double* out);
+void tsd_rng_noise(void* h, size_t n, double* out);
+}
+
+using namespace tsdict;
+
+namespace {
+
+int failures = 0;
+
+void check(const char* name, const std::function<std::string()>& body) {
+  std::string err;
+  try {
+    err = body();
+  } catch (const std::exception& e) {
+    err = std::string("exception: ") + e.what();
+  }
+  std::printf("[%s] %s%s%s\n", err.empty() ? "PASS" : "FAIL", name, err.empty() ? "" : ": ", err.c_str());
+  if (!err.empty()) ++failures;
+}
+
+struct Rng {
+  void* h;
+  explicit Rng(uint64_t s) : h(tsd_rng_new(s)) {}
+  ~Rng() { tsd_rng_free(h); }
+  std::vector<double> walk(size_t n) {
+    std::vector<double> v(n);
+    tsd_rng_walk(h, n, v.data());
+    return v;
+  }
+  std::vector<double> noise(size_t n) {
+    std::vector<double> v(n);
+    tsd_rng_noise(h, n, v.data());
+    return v;
+  }
+};
+
+template <class F>
+std::string expect_code(errc want, F&& f) {
+  try {
+    f();
+  } catch (const error& e) {
+    return e.code() == want ? "" : std::string("wrong code: ") + e.what();
+  }
+  return "no exception";
+}
+
+std::string close_to_oracle(const MatrixProfile& P, const std::vector<double>& rv, const std::vector<int64_t>& ri,
+                            double tol) {
+  if (P.values.size() != rv.size()) return "size mismatch";
+  for (size_t i = 0; i < rv.size(); ++i) {
+    if (std::isinf(rv[i]) != std::isinf(P.values[i])) return "sentinel mismatch at " + std::to_string(i);
+    if (std::isinf(rv[i])) continue;
+    if (std::fabs(P.values[i] - rv[i]) > tol * std::max(1.0, rv[i])) return "value mismatch at " + std::to_string(i);
+    if (P.indices[i] != ri[i] && std::fabs(P.values[i] - rv[i]) > 1e-9)
+      return "index mismatch at " + std::to_string(i);
+  }
+  return "";
+}
+
+}  // namespace
+
+int main() {
+  check("AbJoin.MatchesOracle", [] {
+    Rng r(35);
+    const TimeSeries A{r.noise(300)}, B{r.noise(200)};
+    const MatrixProfile P = ab_join(A, B, 20);
+    std::vector<double> v(281);
+    std::vector<int64_t> i(281);
+    tsdo_ab_join(A.values.data(), 300, B.values.data(), 200, 20, v.data(), i.data());
+    return close_to_oracle(P, v, i, 1e-8);
+  });
+  check("AbJoin.TooShortThrows", [] {
+    Rng r(39);
+    return expect_code(errc::series_too_short, [&] { ab_join(TimeSeries{r.noise(10)}, TimeSeries{r.noise(100)}, 20); });
+  });
+  check("AbJoin.DeterministicAcrossThreadCounts", [] {
+    Rng r(40);
+    const TimeSeries A{r.walk(1500)}, B{r.walk(900)};
+    const auto p1 = ab_join(A, B, 40, 1), p3 = ab_join(A, B, 40, 3);
+    return p1.values == p3.values && p1.indices == p3.indices ? "" : "results differ";
+  });
+  check("SelfJoin.MatchesOracle", [] {
+    Rng r(33);
+    const TimeSeries T{r.walk(2048)};
+    const MatrixProfile P = self_join(T, 50);
+    std::vector<double> v(1999);
+    std::vector<int64_t> i(1999);
+    tsdo_self_join(T.values.data(), 2048, 50, 25, v.data(), i.data());
+    return close_to_oracle(P, v, i, 1e-8);
+  });
+  check("SelfJoin.MinimumLengthEdge", [] {
+    Rng r(31);
+    const MatrixProfile P = self_join(TimeSeries{r.noise(16)}, 8);
+    if (P.values.size() != 9) return std::string("size");
+    if (P.indices[4] != MatrixProfile::no_neighbor || !std::isinf(P.values[4])) return std::string("no sentinel");
+    for (int k : {0, 1, 7, 8})
+      if (P.indices[k] == MatrixProfile::no_neighbor) return std::string("unexpected sentinel");
+    return std::string();
+  });
+  check("SelfJoin.TooShortThrows", [] {
+    Rng r(32);
+    return expect_code(errc::series_too_short, [&] { self_join(TimeSeries{r.noise(15)}, 8); });
+  });
+  check("ComputeStats.Errors", [] {
+    std::string e = expect_code(errc::window_too_large, [] { compute_stats(TimeSeries{{1, 2, 3}}, 4); });
+    if (e.empty()) e = expect_code(errc::window_too_small, [] { compute_stats(TimeSeries{{1, 2, 3}}, 1); });
+    if (e.empty())
+      e = expect_code(errc::non_finite_input, [] { compute_stats(TimeSeries{{1, std::nan(""), 3}}, 2); });
+    return e;
+  });
+  check("ComputeStats.ConstancyMaskIsScaleRelative", [] {
+    std::vector<double> base{5.0, 5.0, 5.0 + 1e-9, 5.0, 1.0, 9.0};
+    auto st = compute_stats(TimeSeries{base}, 4);
+    if (!st.constant_mask[0] || st.constant_mask[2]) return std::string("unscaled mask");
+    for (auto& x : base) x *= 1e6;
+    st = compute_stats(TimeSeries{base}, 4);
+    return st.constant_mask[0] && !st.constant_mask[2] ? std::string() : std::string("scaled mask");
+  });
+  check("JoinDictionary.SingleFullSegmentEqualsAbJoin", [] {
+    Rng r(70);
+    const TimeSeries B{r.walk(600)}, A{r.walk(400)};
+    Dictionary D;
+    D.m = 50;
+    D.source_length = B.n();
+    D.segments.push_back({0, B.values});
+    const auto via_dict = join_dictionary(A, D, 50);
+    const auto direct = ab_join(A, B, 50);
+    return via_dict.values == direct.values && via_dict.indices == direct.indices ? "" : "not bit-identical";
+  });
+  check("JoinDictionary.Errors", [] {
+    Dictionary D;
+    D.m = 40;
+    D.segments.push_back({0, std::vector<double>(100, 1.0)});
+    std::string e = expect_code(errc::window_mismatch, [&] { join_dictionary(TimeSeries{std::vector<double>(200, 0.5)}, D, 41); });
+    Dictionary empty;
+    empty.m = 40;
+    if (e.empty()) e = expect_code(errc::empty_dictionary, [&] { join_dictionary(TimeSeries{std::vector<double>(200)}, empty, 40); });
+    return e;
+  });
+  check("JoinDictionary.IndicesAreSourceCoordinates", [] {
+    Rng r(71);
+    const std::vector<double> src = r.walk(800);
+    const TimeSeries A{r.walk(300)};
+    Dictionary D;
+    D.m = 40;
+    D.source_length = src.size();
+    for (size_t st : {0u, 300u, 610u}) D.segments.push_back({st, std::vector<double>(src.begin() + st, src.begin() + st + 120)});
+    const auto P = join_dictionary(A, D, 40);
+    for (size_t i = 0; i < P.values.size(); ++i) {
+      const auto j = static_cast<size_t>(P.indices[i]);
+      bool inside = false;
+      for (const auto& s : D.segments) inside = inside || (j >= s.start && j + 40 <= s.start + s.length());
+      if (!inside) return "index " + std::to_string(j) + " outside every segment";
+      const double d = tsdo_pair_dist(A.values.data(), A.n(), i, src.data(), src.size(), j, 40);
+      if (std::fabs(d - P.values[i]) > 1e-6) return "value does not match its index at row " + std::to_string(i);
+    }
+    return std::string();
+  });
+  check("EMax.FullCoverageIsZero", [] {
+    Rng r(60);
+    const TimeSeries T{r.walk(500)};
+    Dictionary D;
+    D.m = 50;
+    D.source_length = T.n();
+    D.segments.push_back({0, T.values});
+    const double e = compute_e_max(D, T);
+    return e <= 1e-5 ? "" : "e_max " + std::to_string(e);
+  });
+  std::printf("%d failure(s)\n", failures);
+  return failures;
+}

@@ -1,0 +1,123 @@
+"""Generate tests/golden/reference_cases.npz from the UNMODIFIED reference.
+
+Runs in the build container only (needs /root/reference, compiled into
+oracle/_ref/libtsdict_ref.so by oracle/Makefile). Inputs are drawn with the
+reference's own tests/synth.hpp generators (replaying the seeds and draw
+order of the reference tests cited per case); outputs come from the
+reference's own functions. The fixture is committed; tests read it on any box.
+
+    python tests/golden/make_golden.py
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle import py_oracle as O  # noqa: E402
+
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "reference_cases.npz")
+
+
+def main():
+    if not O.ref_available():
+        raise SystemExit("oracle/_ref/libtsdict_ref.so missing: run `make -C oracle` with /root/reference present")
+    d = {}
+    cases = []
+
+    def stats_case(name, x, m):
+        mu, sd, iv, fl = O.ref_compute_stats(x, m)
+        d[f"{name}__x"], d[f"{name}__m"] = x, np.int64(m)
+        d[f"{name}__means"], d[f"{name}__stds"], d[f"{name}__invn"], d[f"{name}__flat"] = mu, sd, iv, fl
+        cases.append(("stats", name))
+
+    def ab_case(name, a, b, m):
+        v, i = O.ref_ab_join(a, b, m, threads=3)
+        d[f"{name}__a"], d[f"{name}__b"], d[f"{name}__m"] = a, b, np.int64(m)
+        d[f"{name}__val"], d[f"{name}__idx"] = v, i
+        cases.append(("ab", name))
+
+    def self_case(name, t, m):
+        v, i = O.ref_self_join(t, m, threads=3)
+        d[f"{name}__t"], d[f"{name}__m"] = t, np.int64(m)
+        d[f"{name}__val"], d[f"{name}__idx"] = v, i
+        cases.append(("self", name))
+
+    def dict_case(name, q, segs, starts, m):
+        v, i = O.ref_join_dictionary(q, segs, starts, m, threads=3)
+        d[f"{name}__q"], d[f"{name}__m"] = q, np.int64(m)
+        d[f"{name}__seg_vals"] = np.concatenate(segs)
+        d[f"{name}__seg_len"] = np.asarray([len(s) for s in segs], dtype=np.int64)
+        d[f"{name}__seg_start"] = np.asarray(starts, dtype=np.int64)
+        d[f"{name}__val"], d[f"{name}__idx"] = v, i
+        cases.append(("dict", name))
+
+    # stats (test_series.cpp:42-69, :94-105)
+    r = O.RefRng(101)
+    stats_case("stats_noise2048_m64", r.noise(2048), 64)
+    r = O.RefRng(102)
+    stats_case("stats_walk3000_m200", r.walk(3000), 200)
+    stats_case("stats_scale_relative", np.array([5.0, 5.0, 5.0 + 1e-9, 5.0, 1.0, 9.0]), 4)
+    stats_case("stats_constant", np.ones(4), 2)
+    # ab-join (test_profiles.cpp:231-250, :293-301, :215-229, :252-264)
+    r = O.RefRng(35)
+    a = r.noise(300)
+    ab_case("ab_noise_35", a, r.noise(200), 20)
+    r = O.RefRng(36)
+    for t in range(8):
+        A = r.walk(220 + t * 17) if t % 2 == 0 else r.noise(180 + t * 23)
+        B = r.noise(150 + t * 11) if t % 3 == 0 else r.walk(240 - t * 9)
+        ab_case(f"ab_shapes_36_{t}", A, B, 8 + t * 5)
+    r = O.RefRng(40)
+    ab_case("ab_walk_40", r.walk(1500), r.walk(900), 40)
+    r = O.RefRng(34)
+    w = r.walk(300)
+    ab_case("ab_same_content_34", w, w.copy(), 20)
+    A = O.ref_sine(500, 50.0)
+    A[230:250] += 6.0
+    ab_case("ab_planted_spike_37", A, O.ref_sine(600, 50.0), 25)
+    # self-join (test_profiles.cpp:137-193, :206-213)
+    r = O.RefRng(28)
+    self_case("self_noise_28", r.noise(256), 16)
+    r = O.RefRng(29)
+    for t in range(8):
+        n, m = 64 + t * 48, 8 + t * 3
+        T = r.walk(n) if t % 2 == 0 else r.noise(n)
+        if t == 5:
+            T[20:60] = 1.25  # flat stretch (:162)
+        self_case(f"self_shapes_29_{t}", T, m)
+    r = O.RefRng(31)
+    self_case("self_min_length_31", r.noise(16), 8)
+    r = O.RefRng(33)
+    self_case("self_walk_33", r.walk(2048), 50)
+    r = O.RefRng(27)
+    half = r.walk(512)
+    self_case("self_repeated_27", np.concatenate([half, half]), 64)
+    # dictionary joins (test_dict_join.cpp:48-81)
+    r = O.RefRng(70)
+    B = r.walk(600)
+    A = r.walk(400)
+    dict_case("dict_single_full_segment_70", A, [B], [0], 50)
+    r = O.RefRng(71)
+    B = r.walk(800)
+    A = r.walk(300)
+    segs, starts, _ = O.ref_learn_dictionary(B, 40, 0.6)
+    dict_case("dict_learned_71", A, segs, starts, 40)
+    r = O.RefRng(75)
+    B = r.walk(900)
+    A = r.walk(500)
+    segs, starts, _ = O.ref_learn_dictionary(B, 60, 0.0)
+    dict_case("dict_zero_saving_75", A, segs, starts, 60)
+    # BASELINE configs[0] (C1): walk seed 0 (16384) vs 8 walks of 512 (seed 1), m = 100
+    q = O.RefRng(0).walk(16384)
+    rs = O.RefRng(1)
+    segs = [rs.walk(512) for _ in range(8)]
+    dict_case("dict_C1", q, segs, [512 * s for s in range(8)], 100)
+    d["__cases__"] = np.asarray([f"{k}:{n}" for k, n in cases])
+    np.savez_compressed(OUT, **d)
+    print(f"wrote {OUT}: {len(cases)} cases, {os.path.getsize(OUT) / 1024:.0f} KiB")
+
+
+if __name__ == "__main__":
+    main()

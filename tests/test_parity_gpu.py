@@ -1,0 +1,283 @@
+"""GPU parity tests (run on the B200 box: pytest -m gpu).
+
+The CUDA path, called through the C ABI (ctypes mirror of the reference API),
+against (a) the reference's own outputs committed in tests/golden (generated
+by running the unmodified reference, tests/golden/make_golden.py) and (b) the
+oracle restatement at runtime for larger / BASELINE-shaped inputs; full-size
+configs are checked on sampled rows and through size-independent properties.
+Tolerances: tests/parity.py.
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import paper_2112_12965_b200 as tsd
+from paper_2112_12965_b200 import synth
+from oracle import py_oracle as O
+from parity import ab_dist, check_profile, dict_dist
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _segs(c):
+    return np.split(c["seg_vals"], np.cumsum(c["seg_len"])[:-1]), [int(s) for s in c["seg_start"]]
+
+
+def _dict(segs, starts, m):
+    return tsd.Dictionary([tsd.Segment(st, s) for s, st in zip(segs, starts)], m=m,
+                          source_length=max(st + len(s) for s, st in zip(segs, starts)))
+
+
+# ------------------------------------------------------------- golden (reference outputs)
+def test_compute_stats_vs_reference(golden):
+    """test_series.cpp:42-69: means/stds within 1e-9 of the reference; flat mask identical"""
+    for name, (kind, c) in golden.items():
+        if kind != "stats":
+            continue
+        st = tsd.compute_stats(c["x"], int(c["m"]))
+        assert np.max(np.abs(st.means - c["means"])) < 1e-9, name
+        assert np.max(np.abs(st.stds - c["stds"])) < 1e-9, name
+        assert np.array_equal(st.constant_mask, c["flat"]), name
+        nz = c["invn"] > 0
+        assert np.all((st.invn > 0) == nz), name
+        assert np.allclose(st.invn[nz], c["invn"][nz], rtol=1e-9, atol=0), name
+
+
+def test_ab_join_vs_reference(golden):
+    for name, (kind, c) in golden.items():
+        if kind != "ab":
+            continue
+        m = int(c["m"])
+        P = tsd.ab_join(c["a"], c["b"], m)
+        check_profile(P.values, P.indices, c["val"], c["idx"], m, ab_dist(c["a"], c["b"], m), label=name)
+
+
+def test_ab_join_same_content_finds_itself(golden):
+    """test_profiles.cpp:215-229"""
+    c = golden["ab_same_content_34"][1]
+    P = tsd.ab_join(c["a"], c["b"], 20)
+    assert np.all(P.values <= 1e-5)
+
+
+def test_ab_join_planted_spike_is_the_discord(golden):
+    """test_profiles.cpp:252-264"""
+    c = golden["ab_planted_spike_37"][1]
+    P = tsd.ab_join(c["a"], c["b"], 25)
+    assert 206 <= int(np.argmax(P.values)) < 250
+
+
+def test_self_join_vs_reference(golden):
+    for name, (kind, c) in golden.items():
+        if kind != "self":
+            continue
+        m = int(c["m"])
+        P = tsd.self_join(c["t"], m)
+        check_profile(P.values, P.indices, c["val"], c["idx"], m, ab_dist(c["t"], c["t"], m), label=name)
+        ok = P.indices >= 0
+        assert np.all(np.abs(P.indices[ok] - np.nonzero(ok)[0]) > m // 2), f"{name}: exclusion violated"
+
+
+def test_self_join_minimum_length_sentinel(golden):
+    """test_profiles.cpp:181-193: n = 2m with even m -> centre window has no admissible neighbour"""
+    P = tsd.self_join(golden["self_min_length_31"][1]["t"], 8)
+    assert P.indices[4] == -1 and np.isinf(P.values[4])
+    assert all(P.indices[k] != -1 for k in (0, 1, 7, 8))
+
+
+def test_self_join_repeated_content_near_zero(golden):
+    """test_profiles.cpp:137-146"""
+    P = tsd.self_join(golden["self_repeated_27"][1]["t"], 64)
+    assert np.all(P.values[: 512 - 64 + 1] <= 1e-5)
+
+
+def test_dict_join_vs_reference(golden):
+    for name, (kind, c) in golden.items():
+        if kind != "dict":
+            continue
+        m = int(c["m"])
+        segs, starts = _segs(c)
+        P = tsd.join_dictionary(c["q"], _dict(segs, starts, m), m)
+        check_profile(P.values, P.indices, c["val"], c["idx"], m, dict_dist(c["q"], segs, starts, m), label=name)
+
+
+def test_single_full_segment_equals_ab_join_bitwise(golden):
+    """test_dict_join.cpp:48-60: the dictionary path and ab_join share code"""
+    c = golden["dict_single_full_segment_70"][1]
+    segs, starts = _segs(c)
+    via = tsd.join_dictionary(c["q"], _dict(segs, starts, 50), 50)
+    direct = tsd.ab_join(c["q"], segs[0], 50)
+    assert np.array_equal(via.values, direct.values) and np.array_equal(via.indices, direct.indices)
+
+
+def test_exact_recovery_at_zero_saving(golden):
+    """test_dict_join.cpp:181-192: a zero-saving dictionary reproduces the exact join to 1e-9"""
+    c = golden["dict_zero_saving_75"][1]
+    segs, starts = _segs(c)
+    B = np.concatenate(segs)
+    approx = tsd.join_dictionary(c["q"], _dict(segs, starts, 60), 60)
+    exact = tsd.ab_join(c["q"], B, 60)
+    assert np.max(np.abs(approx.values - exact.values)) <= 1e-9
+
+
+# ------------------------------------------------------------- oracle at runtime
+@pytest.mark.parametrize("seed,na,nb,m", [(1, 5000, 3000, 100), (2, 20000, 4096, 100), (3, 3000, 2500, 7),
+                                         (4, 8000, 1100, 512), (5, 1200, 70000, 64)])
+def test_ab_join_vs_oracle_walks(seed, na, nb, m):
+    a, b = synth.walk(seed, na), synth.walk(seed + 100, nb)
+    P = tsd.ab_join(a, b, m)
+    rv, ri = O.ab_join(a, b, m)
+    check_profile(P.values, P.indices, rv, ri, m, ab_dist(a, b, m), label=f"ab{seed}")
+
+
+@pytest.mark.parametrize("excl", [None, 62, 0, 300])
+def test_self_join_exclusion_parameter_ecg(excl):
+    """BASELINE C2 shape (ECG-like, m=250) at reduced n: excl = m/4 (62) via the
+    one-constant restatement, m/2 via the reference rule"""
+    t, _ = synth.ecg(2, 12000)
+    m = 250
+    P = tsd.self_join(t, m, excl=excl)
+    rv, ri = O.self_join(t, m, excl)
+    check_profile(P.values, P.indices, rv, ri, m, ab_dist(t, t, m), label=f"self excl={excl}")
+
+
+def test_flat_windows_ab_and_self():
+    """flat stretches in query and target (profiles.hpp:290-294, :331-336)"""
+    a = synth.Rng(9).noise(2000)
+    a[300:500] = 2.5
+    b = synth.Rng(10).noise(1500)
+    b[700:800] = -1.0
+    for m in (16, 64):
+        P = tsd.ab_join(a, b, m)
+        rv, ri = O.ab_join(a, b, m)
+        check_profile(P.values, P.indices, rv, ri, m, ab_dist(a, b, m), label=f"flat ab m={m}")
+        P = tsd.self_join(a, m)
+        rv, ri = O.self_join(a, m)
+        check_profile(P.values, P.indices, rv, ri, m, ab_dist(a, a, m), label=f"flat self m={m}")
+        P = tsd.ab_join(a, synth.Rng(11).noise(900), m)  # flat rows, no flat column
+        rv, ri = O.ab_join(a, synth.Rng(11).noise(900), m)
+        check_profile(P.values, P.indices, rv, ri, m, label=f"flat rows only m={m}")
+
+
+def test_dict_join_C3_shape_reduced():
+    """BASELINE C3 shape: ECG query with anomalous beats vs 32 segments x 2048, m = 200
+    (query reduced to 2^15 samples so the oracle finishes in seconds)"""
+    q, _ = synth.ecg(3, 1 << 15, 4)
+    train, _ = synth.ecg(13, 32 * 2048 * 4)
+    segs = [train[k * 8192: k * 8192 + 2048] for k in range(32)]
+    starts = [k * 8192 for k in range(32)]
+    m = 200
+    P = tsd.join_dictionary(q, _dict(segs, starts, m), m)
+    rv, ri = O.dict_join(q, segs, starts, m)
+    check_profile(P.values, P.indices, rv, ri, m, dict_dist(q, segs, starts, m), label="C3 reduced")
+
+
+def test_batched_C5_shape():
+    """BASELINE C5 shape: transport-like series vs one shared 64 x 1024 dictionary,
+    m = 128, one device pass; each series equals its own join_dictionary oracle"""
+    series = synth.traffic(6, 24, 8192)
+    src = synth.traffic(16, 1, 65536 * 2)[0]
+    segs = [src[k * 2048: k * 2048 + 1024] for k in range(64)]
+    starts = [k * 2048 for k in range(64)]
+    m = 128
+    D = _dict(segs, starts, m)
+    outs = tsd.join_dictionary_batched(list(series), D, m)
+    assert len(outs) == 24
+    for k in (0, 7, 23):
+        rv, ri = O.dict_join(series[k], segs, starts, m)
+        check_profile(outs[k].values, outs[k].indices, rv, ri, m, dict_dist(series[k], segs, starts, m),
+                      label=f"C5 series {k}")
+    rng = np.random.default_rng(0)
+    for k in rng.choice(24, 6, replace=False):  # sampled rows of the others
+        for i in rng.choice(8192 - m + 1, 4, replace=False):
+            rv, ri = O.dict_join(series[k][i:i + m], segs, starts, m)
+            check_profile(outs[k].values[i:i + 1], outs[k].indices[i:i + 1], rv, ri, m,
+                          dict_dist(series[k][i:i + m], segs, starts, m), label=f"C5 s{k} row {i}")
+
+
+def test_C4_full_size_row_sampled_and_properties():
+    """BASELINE C4 at full size (2^24 x 256 x 1024, m = 512): 48 sampled rows
+    against the oracle (ab_join of the single window vs every segment), plus
+    size-independent properties over all 16.8M rows."""
+    import bench
+    D, segs = bench.make_dictionary()
+    q = bench.make_query(bench.Q_SEED)
+    m = bench.M
+    P = tsd.join_dictionary(q, D, m)
+    n = q.size - m + 1
+    assert P.values.shape == (n,)
+    assert np.all(np.isfinite(P.values)) and np.all(P.values >= 0) and np.all(P.values <= 2 * np.sqrt(m))
+    local = P.indices % bench.SEG_LEN
+    assert np.all(local <= bench.SEG_LEN - m), "an index points at a straddling window"
+    starts = [bench.SEG_LEN * s for s in range(bench.N_SEG)]
+    rng = np.random.default_rng(1)
+    rows = np.concatenate([[0, 1, n - 1, 16383, 16384], rng.choice(n, 43, replace=False)])
+    for i in rows:
+        rv, ri = O.dict_join(q[i:i + m], list(segs), starts, m)
+        check_profile(P.values[i:i + 1], P.indices[i:i + 1], rv, ri, m, dict_dist(q[i:i + m], list(segs), starts, m),
+                      label=f"C4 row {i}")
+    # monotone refinement (test_dict_join.cpp:194-221): dropping segments never lowers a value
+    sub = tsd.Dictionary(D.segments[::2], m=m, source_length=D.source_length)
+    Q = q[: 1 << 20]
+    full = tsd.join_dictionary(Q, D, m)
+    half = tsd.join_dictionary(Q, sub, m)
+    assert np.all(full.values <= half.values + 1e-9)
+    # the prefix query runs with another task decomposition (different edge
+    # rows), so it matches the full run to rounding, not bitwise
+    check_profile(full.values, full.indices, P.values[: full.values.size], P.indices[: full.indices.size], m,
+                  dict_dist(Q, list(segs), starts, m), label="C4 prefix vs full")
+
+
+def test_deterministic_repeat_and_plan_paths():
+    """bit-identical across repeats, host/device plan entry points and threads"""
+    import torch
+    q = synth.walk(21, 200000)
+    segs = list(synth.walks(22, 16, 1024))
+    D = _dict(segs, [1024 * s for s in range(16)], 300)
+    a = tsd.join_dictionary(q, D, 300, threads=1)
+    b = tsd.join_dictionary(q, D, 300, threads=7)
+    assert np.array_equal(a.values, b.values) and np.array_equal(a.indices, b.indices)
+    plan = tsd.DictPlan(D, 300)
+    dq = torch.from_numpy(q).cuda()
+    dv = torch.empty(q.size - 299, dtype=torch.float64, device="cuda")
+    di = torch.empty(q.size - 299, dtype=torch.int64, device="cuda")
+    plan.join_device(dq.data_ptr(), [q.size], dv.data_ptr(), di.data_ptr())
+    assert np.array_equal(dv.cpu().numpy(), a.values) and np.array_equal(di.cpu().numpy(), a.indices)
+    hv, hi = np.empty(q.size - 299), np.empty(q.size - 299, dtype=np.int64)
+    plan.join_host(q, [q.size], hv, hi)
+    assert np.array_equal(hv, a.values) and np.array_equal(hi, a.indices)
+
+
+def test_errors_on_device_path():
+    with pytest.raises(tsd.TsdictError) as ei:
+        x = np.random.rand(500)
+        x[123] = np.nan
+        tsd.ab_join(x, np.random.rand(300), 20)
+    assert ei.value.code() == tsd.errc.non_finite_input
+    with pytest.raises(tsd.TsdictError) as ei:
+        seg = np.random.rand(300)
+        seg[5] = np.inf
+        tsd.join_dictionary(np.random.rand(500), tsd.Dictionary([tsd.Segment(0, seg)], m=20), 20)
+    assert ei.value.code() == tsd.errc.non_finite_input
+
+
+def test_compute_e_max():
+    """dictionary.hpp:247-255 and test_dictionary.cpp:416-442"""
+    t = synth.Rng(60).walk(500)
+    assert tsd.compute_e_max(tsd.Dictionary([tsd.Segment(0, t)], m=50, source_length=500), t) <= 1e-5
+    x = synth.sine(512, 32.0)
+    both = np.concatenate([x, x])
+    D = tsd.Dictionary([tsd.Segment(0, both[:512])], m=64, source_length=1024)
+    assert tsd.compute_e_max(D, both) <= 1e-6
+
+
+def test_cpp_dropin_headers():
+    """include/tsdict/*.hpp used like the reference's own GoogleTest suites"""
+    exe = os.path.join(ROOT, "tests", "cpp", "build", "test_dropin")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "[FAIL]" not in r.stdout
