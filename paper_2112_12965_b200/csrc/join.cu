@@ -69,7 +69,8 @@ struct JoinArgs {
   const uint8_t* flag_a;
   const double* xb;
   const double* mub;
-  const double4* col;  // {df, dg, invn, 0} per concatenated column (padded by 64)
+  const double4* col;   // normalised-recurrence column data (k_pack_cols), padded by 64
+  const double* scale;  // s_j per concatenated column
   const SegDev* segs;
   const int* seg_eoff;  // compact edge offset of each segment inside its group (even)
   const double* btil;   // [nseg][m] centred samples of each segment's window 0
@@ -95,6 +96,10 @@ struct __align__(16) WarpSmem {
   double unif[T];
 };
 
+#ifdef TSD_COUNT_EXACT
+__device__ unsigned long long g_exact_count, g_step_count, g_exact_first, g_step_first;
+#endif
+
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void cp16(void* sdst, const void* gsrc) {
@@ -113,14 +118,28 @@ __device__ __forceinline__ double shfl_up1(double v) {
   return __hiloint2double(hi, lo);
 }
 
-__device__ __forceinline__ bool vote_any(bool p) {
+// warp vote over R = 8 slot tests "hi(c~) >= thr": two independent 4-deep
+// predicate chains joined by one OR (ptxas otherwise builds one 8-deep chain)
+template <int R>
+__device__ __forceinline__ bool vote_any8(const double (&P)[R], int ph, const int (&thr)[R]) {
+  static_assert(R == 8, "vote_any8 is written for R = 8");
   unsigned r;
   asm volatile(
-      "{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n vote.sync.any.pred q, q, -1;\n selp.u32 %0, 1, 0, q;\n}\n"
+      "{\n .reg .pred a, b;\n"
+      " setp.ge.s32 a, %1, %9;\n setp.ge.s32 b, %5, %13;\n"
+      " setp.ge.or.s32 a, %2, %10, a;\n setp.ge.or.s32 b, %6, %14, b;\n"
+      " setp.ge.or.s32 a, %3, %11, a;\n setp.ge.or.s32 b, %7, %15, b;\n"
+      " setp.ge.or.s32 a, %4, %12, a;\n setp.ge.or.s32 b, %8, %16, b;\n"
+      " or.pred a, a, b;\n vote.sync.any.pred a, a, -1;\n selp.u32 %0, 1, 0, a;\n}\n"
       : "=r"(r)
-      : "r"((unsigned)p));
+      : "r"(__double2hiint(P[(0 + ph) & 7])), "r"(__double2hiint(P[(1 + ph) & 7])),
+        "r"(__double2hiint(P[(2 + ph) & 7])), "r"(__double2hiint(P[(3 + ph) & 7])),
+        "r"(__double2hiint(P[(4 + ph) & 7])), "r"(__double2hiint(P[(5 + ph) & 7])),
+        "r"(__double2hiint(P[(6 + ph) & 7])), "r"(__double2hiint(P[(7 + ph) & 7])), "r"(thr[0]), "r"(thr[1]),
+        "r"(thr[2]), "r"(thr[3]), "r"(thr[4]), "r"(thr[5]), "r"(thr[6]), "r"(thr[7]));
   return r != 0;
 }
+
 
 // out[r] = sum_{t<m} U[t] * (S[R*lane + r + t] - cS), U[t] = Ug[t] - cu.
 // S samples at index >= s_avail read as cS (contribute 0). Returns sum U in *esum.
@@ -181,6 +200,7 @@ struct SweepCtx {
   long long row0;  // row of this lane's slot 0
   long long excl;  // self-join exclusion half-width
   bool write_out;
+  bool first_seg;  // diagnostics only
 };
 
 // chunk c of the segment: column data for steps [32c, 32c+32) -> colbuf[c%3],
@@ -201,58 +221,38 @@ __device__ __forceinline__ void flush_block(WarpSmem<R>& sm, const SweepCtx& cx,
   if (j < cx.ncol - 1) cx.E[j] = sm.ering[(b % 3) * 32 + lane];
 }
 
-// Per-slot test threshold for a block: the high word of bestK * min_norm_b
-// over the block's columns, minus one. cov*invn_b > bestK implies
-// cov > bestK * norm_b >= bestK * min_norm_b, so hi(cov) >= thr whenever the
-// cell can improve the row (bestK > 0); bestK <= 0 (no positive candidate
-// yet) passes everything, inactive rows carry bestK = +inf and never pass.
-__device__ __forceinline__ int block_thr(double bK, double mnorm) {
-  const int h = __double2hiint(bK * mnorm);
+// Test threshold of a slot: high word of its best K minus one (a candidate
+// can only win with hi(K) >= hi(bestK) - 1, so the integer test on K's high
+// word is conservative); bestK <= 0 passes everything (rare: no positive
+// candidate yet), inactive rows carry bestK = +inf and never pass.
+__device__ __forceinline__ int slot_thr(double bK) {
+  const int h = __double2hiint(bK);
   return h > 0 ? h - 1 : INT_MIN;
 }
 
+// Column data of one step: df_b * s, dg_b * s, s_k / s_{k-1}, and the factor
+// invn_b / s (1, or 0 for a flat column) -- see k_pack_cols.
 struct StepIn {
-  double dfb, dgb, e, in;
+  double dfb, dgb, rk, kf, e, in;
 };
 
 __device__ __forceinline__ void prefetch(const double4* cb, const double* ep, double v7, StepIn& d) {
-  const double2 dd = *reinterpret_cast<const double2*>(cb);
-  d.dfb = dd.x;
-  d.dgb = dd.y;
+  const double4 c = *cb;
+  d.dfb = c.x;
+  d.dgb = c.y;
+  d.rk = c.z;
+  d.kf = c.w;
   d.e = *ep;
   d.in = shfl_up1(v7);
 }
 
 template <int R>
 struct SweepState {
-  double P[R];  // slot registers: step k, slot r at P[(r - k) mod R]
-  int thr[R];   // high-word test thresholds of the current block
-  StepIn nx;    // prefetched inputs of the next step
+  double P[R];   // slot registers: step k, slot r at P[(r - k) mod R]
+  double bK[R];  // best K = cov * invn_b per slot (row factor invn_a left out)
+  int thr[R];    // slot_thr(bK); the best column lives in sm.bj (written on update only)
+  StepIn nx;     // prefetched inputs of the next step
 };
-
-// Exact update (taken by the warp when some lane's coarse test passed):
-// K = cov * invn_b for every slot, full double compare with the slot's best
-// K; columns arrive in increasing order, so ties keep the earlier (lower)
-// column (profiles.hpp:70-77).
-template <int R, bool SELF>
-__device__ __forceinline__ void exact_step(WarpSmem<R>& sm, int lane, const SweepState<R>& S, int ph, double ivb,
-                                           double mnorm, int col, long long row0, long long excl, int (&thr)[R]) {
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const double cov = S.P[(r + ph) & (R - 1)];
-    bool ok = __double2hiint(cov) >= thr[r];
-    if (SELF) {
-      const long long d = row0 + r - col;
-      ok = ok && (d > excl || d < -excl);  // profiles.hpp:281-284
-    }
-    const double K = cov * ivb;
-    if (ok && K > sm.bK[r][lane]) {
-      sm.bK[r][lane] = K;
-      sm.bj[r][lane] = col;
-      thr[r] = block_thr(K, mnorm);
-    }
-  }
-}
 
 // One block of R steps starting at k0 (k0 % R == 0, R | 32). FIRST: block 0,
 // whose step 0 (heads, already in P) only needs its test. GUARD: steps may
@@ -268,48 +268,70 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
   const int ebase = k0 % 96;                       // ring position of E[k0]
   double* const st_prev = sbase + (k0 + 95) % 96;  // E[k0-1]
   double* const st_cur = sbase + ebase;
-  const double mnorm = ccur->w;  // min norm_b over this block's columns
-#pragma unroll
-  for (int r = 0; r < R; ++r) S.thr[r] = block_thr(sm.bK[r][lane], mnorm);
 #pragma unroll
   for (int u = 0; u < R; ++u) {
     const int k = k0 + u;
     if (GUARD && k >= n) break;
     const int ph = (R - u) & (R - 1);  // physical register of slot 0 at this step
+    const double kf = S.nx.kf;         // invn_b / s (1, or 0 for a flat column)
     if (!(FIRST && u == 0)) {
       // fold in the incoming diagonal; lane 31 retires its bottom-row value (column k-1)
       (u == 0 ? st_prev : st_cur + u - 1)[0] = S.P[ph];
       S.P[ph] = l0 ? S.nx.e : S.nx.in;
-      const double dfb = S.nx.dfb, dgb = S.nx.dgb;
+      const double dfb = S.nx.dfb, dgb = S.nx.dgb, rk = S.nx.rk;
+      // normalised recurrence c~(i,k) = c~(i-1,k-1) * s_k / s_{k-1} + (df_a dg_b + dg_a df_b) * s_k
+      // (profiles.hpp:330 scaled by s_k = invn_b[k]); only the last FMA depends on the previous step
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         double& c = S.P[(r + ph) & (R - 1)];
-        c = __fma_rn(dfa[r], dgb, c);
-        c = __fma_rn(dga[r], dfb, c);
+        const double t = __fma_rn(dfa[r], dgb, dga[r] * dfb);
+        c = __fma_rn(c, rk, t);
       }
     }
     if (!GUARD || k + 1 < n)
       prefetch(u + 1 < R ? ccur + u + 1 : cnext, &sm.ering[ebase + u], S.P[(ph + R - 1) & (R - 1)], S.nx);
+    // c~ = cov * invn_b = K for non-flat columns: test its high word directly
     bool p[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) p[r] = __double2hiint(S.P[(r + ph) & (R - 1)]) >= S.thr[r];
+#ifdef TSD_ABL_NOEXACT
+    if (vote_any8(S.P, ph, S.thr) && cx.ncol < 0) [[unlikely]] {
+#else
+    if (vote_any8(S.P, ph, S.thr)) [[unlikely]] {
+#endif
+#ifdef TSD_COUNT_EXACT
+      if (lane == 0) atomicAdd(&g_exact_count, 1ull);
+      if (lane == 0 && cx.first_seg) atomicAdd(&g_exact_first, 1ull);
+#endif
+      // exact update: strict K > bestK (columns arrive in increasing order,
+      // so ties keep the lower column, profiles.hpp:70-77); flat column -> K = 0
+      const int col = cx.colbase + k;
 #pragma unroll
-    for (int w = 1; w < R; w <<= 1)
-#pragma unroll
-      for (int r = 0; r + w < R; r += 2 * w) p[r] = p[r] | p[r + w];
-    if (__builtin_expect(vote_any(p[0]), 0))
-      exact_step<R, SELF>(sm, lane, S, ph, (ccur + u)->z, mnorm, cx.colbase + k, cx.row0, cx.excl, S.thr);
+      for (int r = 0; r < R; ++r) {
+        const double K = S.P[(r + ph) & (R - 1)] * kf;
+        bool ok = K > S.bK[r] && (p[r] || kf == 0.0);
+        if (SELF) {
+          const long long d = cx.row0 + r - col;
+          ok = ok && (d > cx.excl || d < -cx.excl);  // profiles.hpp:281-284
+        }
+        if (ok) {
+          S.bK[r] = K;
+          sm.bj[r][lane] = col;
+          S.thr[r] = slot_thr(K);
+        }
+      }
+    }
   }
 }
 
 // Software-pipelined sweep of one segment. Per step: fold in the incoming
 // diagonal, 2 DFMA per slot, prefetch the next step's column data / edge /
-// shuffle, then the high-word test of every slot against its block threshold
-// (no per-cell multiply) and one warp vote.
+// shuffle, K = cov * invn_b, the high-word test of every slot against its
+// threshold and one warp vote; the exact update runs only on a pass.
 template <int R, bool SELF>
 __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, const double (&dfa)[R],
                               const double (&dga)[R], SweepState<R>& S) {
-  static_assert(R == 8 || R == 16, "R must be 8 or 16");
+  static_assert(R == 8, "the sweep is written for R = 8 rows per lane");
   const int n = cx.ncol;
   const int nchunks = (n + 31) >> 5;
   double* const sbase = lane == 31 ? sm.ering : sm.edummy;  // lane 31 stores into the ring
@@ -320,7 +342,7 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   cp_wait<1>();
   __syncwarp();
   int flushed = 0;  // edge blocks [0, flushed) written back
-  if (n > 1) prefetch(&sm.colbuf[0][1], &sm.ering[0], S.P[R - 1], S.nx);
+  S.nx.kf = sm.colbuf[0][0].w;  // step 0 (heads) only needs the flat factor
   auto chunk_turn = [&](int k0) {
     // the block after this one opens chunk c: make it resident, retire edge
     // block c-2, start loading chunk c+1 (3-deep rings keep in-use slots intact)
@@ -333,7 +355,9 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
       }
       __syncwarp();
       if (c + 1 < nchunks) issue_chunk(sm, cx, lane, c + 1); else cp_commit();
+#ifndef TSD_ABL_NOWAIT
       cp_wait<1>();
+#endif
       __syncwarp();
     }
   };
@@ -354,6 +378,10 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   }
   cp_wait<0>();
   __syncwarp();
+#ifdef TSD_COUNT_EXACT
+  if (lane == 0) atomicAdd(&g_step_count, (unsigned long long)n);
+  if (lane == 0 && cx.first_seg) atomicAdd(&g_step_first, (unsigned long long)n);
+#endif
   if (cx.write_out) {
     const int last = (n - 2) >> 5;  // last edge block holding j <= n-2
     for (int b = flushed; b <= last && n >= 2; ++b) flush_block(sm, cx, lane, b);
@@ -399,6 +427,7 @@ __global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join
         cx.write_out = (b + 1 < b1);
         cx.row0 = i0 + R * lane;
         cx.excl = a.excl;
+        cx.first_seg = (s == s_beg);
         if (b == b0 && sg.ncol >= 2) {
           // top edge of the task: E[j] = cov(re, j + delta), j = 0 .. ncol-2
           // (row 0 has df = dg = 0, so E[j] = cov(0, j+1) feeds it exactly)
@@ -413,7 +442,11 @@ __global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               const int q = q0 + R * lane + r;
-              if (q < sg.ncol - 1 + delta) cx.E[q - delta] = out[r] - (a.mub[sg.col0 + q] - cS) * eU;
+              // stored in the scale of column q - delta: the consumer multiplies
+              // by s_{k}/s_{k-1} (delta = 1: row 0 adds nothing, so c~(0,q) =
+              // E[q-1] * s_q / s_{q-1} must hold)
+              if (q < sg.ncol - 1 + delta)
+                cx.E[q - delta] = (out[r] - (a.mub[sg.col0 + q] - cS) * eU) * a.scale[sg.col0 + q - delta];
             }
           }
           __threadfence_block();
@@ -422,16 +455,22 @@ __global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join
         SweepState<R> S;
         {  // left edge: cov(i, col0) for the band's rows
           double out[R];
+#ifdef TSD_ABL_NOHEADS
+#pragma unroll
+          for (int r = 0; r < R; ++r) out[r] = 0.0;
+#else
           sliding_dot<R>(sm, a.btil + (int64_t)s * a.m, 0.0, a.xa + i0, a.na - i0, cA, a.m, lane, out, nullptr);
-          const double e = a.ebt[s];
+#endif
+          const double e = a.ebt[s], s0 = a.scale[sg.col0];
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const int64_t i = i0 + R * lane + r;
             const double mu = i < a.nrows ? a.mua[i] : cA;
-            S.P[r] = out[r] - (mu - cA) * e;
+            S.P[r] = (out[r] - (mu - cA) * e) * s0;
           }
         }
-        // row data (reloaded per segment so it is not live across the heads)
+        // row data and row bests (reloaded per segment so they are not live
+        // across the heads)
         double dfa[R], dga[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -439,8 +478,12 @@ __global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join
           const bool in = i < a.nrows;
           dfa[r] = in ? a.dfa[i] : 0.0;
           dga[r] = in ? a.dga[i] : 0.0;
+          S.bK[r] = sm.bK[r][lane];
+          S.thr[r] = slot_thr(S.bK[r]);
         }
         sweep_segment<R, SELF>(sm, cx, lane, dfa, dga, S);
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm.bK[r][lane] = S.bK[r];
       }
       // band results: c = clamp(K * invn_a) (profiles.hpp:331, :335)
       double* oc = a.out_c + (int64_t)g * a.nrows;
@@ -478,20 +521,27 @@ __global__ void k_merge_groups(double* __restrict__ c, int64_t* __restrict__ j, 
   j[i] = bj;
 }
 
-// column data {df, dg, invn, min norm over the next R columns} (norm = 1/invn,
-// +inf for flat / straddling windows); the sweep reads .w at block starts
+// Column data for the normalised recurrence (one double4 per concatenated
+// column j): the sweep tracks c~(i,j) = cov(i,j) * s_j with s_j = invn_b[j]
+// (s_j = 1 for flat or straddling windows, so the scale never vanishes):
+//   {df_b[j] * s_j, dg_b[j] * s_j, s_j / s_{j-1}, invn_b[j] / s_j}
+// and scale[j] = s_j for the heads / top edges.
 __global__ void k_pack_cols(const double* __restrict__ df, const double* __restrict__ dg,
-                            const double* __restrict__ invn, int64_t n, int R, double4* __restrict__ col) {
+                            const double* __restrict__ invn, int64_t n, double4* __restrict__ col,
+                            double* __restrict__ scale) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n + 64) return;
-  const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  double mn = inf;
-  for (int q = 0; q < R; ++q) {
-    const int64_t j = i + q;
-    const double iv = j < n ? invn[j] : 0.0;
-    if (iv > 0.0) mn = fmin(mn, 1.0 / iv);
+  if (i >= n) {
+    col[i] = make_double4(0, 0, 1, 0);
+    scale[i] = 1.0;
+    return;
   }
-  col[i] = i < n ? make_double4(df[i], dg[i], invn[i], mn) : make_double4(0, 0, 0, mn);
+  const double iv = invn[i];
+  const double sj = iv > 0.0 ? iv : 1.0;
+  const double ivp = i > 0 ? invn[i - 1] : 0.0;
+  const double sp = ivp > 0.0 ? ivp : 1.0;
+  col[i] = make_double4(df[i] * sj, dg[i] * sj, sj / sp, iv > 0.0 ? 1.0 : 0.0);
+  scale[i] = sj;
 }
 
 __global__ void k_btil(const double* __restrict__ xb, const double* __restrict__ mub, const SegDev* __restrict__ segs,
@@ -716,12 +766,13 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   int* d_eoff = (int*)arena.get(sizeof(int) * nseg);
   int* d_gs = (int*)arena.get(sizeof(int) * (G + 1));
   double4* d_col = (double4*)arena.get(sizeof(double4) * (in.cols.nwin + 64));
+  double* d_scale = (double*)arena.get(sizeof(double) * (in.cols.nwin + 64));
   double* d_btil = (double*)arena.get(sizeof(double) * (int64_t)nseg * m);
   double* d_ebt = (double*)arena.get(sizeof(double) * nseg);
   double* d_edges = (double*)arena.get(sizeof(double) * ecap * used_warps);
   double* d_pc = G > 1 ? (double*)arena.get(sizeof(double) * nrows * G) : d_best_c;
   int64_t* d_pj = G > 1 ? (int64_t*)arena.get(sizeof(int64_t) * nrows * G) : d_best_j;
-  if (!d_segs || !d_eoff || !d_gs || !d_col || !d_btil || !d_ebt || !d_edges || !d_pc || !d_pj) {
+  if (!d_segs || !d_eoff || !d_gs || !d_col || !d_scale || !d_btil || !d_ebt || !d_edges || !d_pc || !d_pj) {
     if (err) *err = Error{kCudaError, "device allocation failed for the join"};
     return kCudaError;
   }
@@ -730,7 +781,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   CUDA_TRY(cudaMemcpyAsync(d_gs, group_seg.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice, st));
   int nl = 0;
   k_pack_cols<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(in.cols.df, in.cols.dg, in.cols.invn,
-                                                                          in.cols.nwin, R, d_col);
+                                                                          in.cols.nwin, d_col, d_scale);
   ++nl;
   k_btil<<<nseg, 128, 0, st>>>(in.xb, in.cols.mu, d_segs, m, d_btil, d_ebt);
   ++nl;
@@ -746,6 +797,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   a.xb = in.xb;
   a.mub = in.cols.mu;
   a.col = d_col;
+  a.scale = d_scale;
   a.segs = d_segs;
   a.seg_eoff = d_eoff;
   a.btil = d_btil;
@@ -761,8 +813,29 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   a.edges = d_edges;
   a.out_c = d_pc;
   a.out_j = d_pj;
+#ifdef TSD_COUNT_EXACT
+  unsigned long long zero = 0;
+  cudaMemcpyToSymbol(g_exact_count, &zero, 8);
+  cudaMemcpyToSymbol(g_step_count, &zero, 8);
+  cudaMemcpyToSymbol(g_exact_first, &zero, 8);
+  cudaMemcpyToSymbol(g_step_first, &zero, 8);
+#endif
   kern<<<grid, 32 * WARPS, smem_bytes, st>>>(a);
   ++nl;
+#ifdef TSD_COUNT_EXACT
+  {
+    unsigned long long ce = 0, cs = 0;
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(&ce, g_exact_count, 8);
+    cudaMemcpyFromSymbol(&cs, g_step_count, 8);
+    unsigned long long cef = 0, csf = 0;
+    cudaMemcpyFromSymbol(&cef, g_exact_first, 8);
+    cudaMemcpyFromSymbol(&csf, g_step_first, 8);
+    fprintf(stderr, "[tsd] exact-path steps %llu of %llu warp-steps (%.2f%%); first segment %.2f%%, others %.2f%%\n",
+            ce, cs, 100.0 * ce / (cs ? cs : 1), 100.0 * cef / (csf ? csf : 1),
+            100.0 * (ce - cef) / ((cs - csf) ? (cs - csf) : 1));
+  }
+#endif
   if (G > 1) {
     k_merge_groups<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(d_pc, d_pj, nrows, G);
     ++nl;
@@ -774,11 +847,6 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   return kOk;
 }
 
-int rows_per_lane() {
-  const char* e = getenv("TSD_ROWS_PER_LANE");
-  return (e && atoi(e) == 16) ? 16 : 8;
-}
-
 }  // namespace
 
 int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st, Error* err,
@@ -788,9 +856,6 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     return kInvalidArgument;
   }
   const bool self = in.excl >= 0;
-  if (rows_per_lane() == 16)
-    return self ? launch_join<16, true>(in, d_best_c, d_best_j, arena, st, err, launches)
-                : launch_join<16, false>(in, d_best_c, d_best_j, arena, st, err, launches);
   return self ? launch_join<8, true>(in, d_best_c, d_best_j, arena, st, err, launches)
               : launch_join<8, false>(in, d_best_c, d_best_j, arena, st, err, launches);
 }

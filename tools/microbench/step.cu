@@ -1,0 +1,138 @@
+// Synthetic replica of one sweep step of k_join_f64 (R = 8 slots/lane) to
+// find the inner-loop bottleneck. VAR bits: 1 = shuffle + lane-0 select,
+// 2 = high-word test + predicate tree + vote + (never taken) branch,
+// 4 = shared-memory loads/store of the step, 8 = deferred-vote style (vote of
+// step k resolved after step k+1's DFMAs, via two register sets).
+#include <cstdio>
+#include <cuda_runtime.h>
+constexpr int R = 8;
+
+__device__ __forceinline__ double shfl_up1(double v) {
+  int lo = __double2loint(v), hi = __double2hiint(v);
+  asm volatile("shfl.sync.up.b32 %0, %0, 1, 0, -1;\n" : "+r"(lo));
+  asm volatile("shfl.sync.up.b32 %0, %0, 1, 0, -1;\n" : "+r"(hi));
+  return __hiloint2double(hi, lo);
+}
+__device__ __forceinline__ bool vote_any(bool p) {
+  unsigned r;
+  asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %1, 0;\n vote.sync.any.pred q, q, -1;\n selp.u32 %0, 1, 0, q;\n}\n"
+               : "=r"(r) : "r"((unsigned)p));
+  return r != 0;
+}
+
+template <int VAR>
+__global__ void __launch_bounds__(64, 8) k(double* out, int steps, int* hits) {
+  __shared__ double sm[2][8][64];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double P[R], dfa[R], dga[R];
+  int thr[R];
+  for (int r = 0; r < R; ++r) {
+    P[r] = lane * 0.01 + r;
+    dfa[r] = 1e-3 * (r + 1);
+    dga[r] = -1e-3 * (r + 2);
+    thr[r] = 0x7fe00000;
+  }
+  for (int i = threadIdx.x; i < 8 * 64; i += blockDim.x) { sm[0][0][i] = 1e-4 * i; }
+  __syncthreads();
+  double dfb = 0.5, dgb = 0.25, e = 1.0;
+  int cnt = 0;
+  bool pend = false;
+  for (int s = 0; s < steps; s += R) {
+#pragma unroll
+    for (int u = 0; u < R; ++u) {
+      const int ph = (R - u) & (R - 1);
+      if (VAR & 4) {
+        const double2 dd = *reinterpret_cast<const double2*>(&sm[w][u][2 * (s & 15)]);
+        dfb = dd.x; dgb = dd.y;
+        e = sm[w][u ^ 1][lane & 7];
+        sm[w][u][32 + (lane & 7)] = P[ph];
+      }
+      if (VAR & 1) {
+        const double in = shfl_up1(P[ph]);
+        P[ph] = lane == 0 ? e : in;
+      }
+      if (VAR & 16) {  // normalised recurrence: 3 FP64 ops per cell, one on the chain
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          double& c = P[(r + ph) & (R - 1)];
+          const double t = __fma_rn(dfa[r], dgb, dga[r] * dfb);
+          c = __fma_rn(c, 0.999999, t);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          double& c = P[(r + ph) & (R - 1)];
+          c = __fma_rn(dfa[r], dgb, c);
+          c = __fma_rn(dga[r], dfb, c);
+        }
+      }
+      if (VAR & 8) {  // deferred: resolve the previous step's vote after this step's math
+        if (pend) {
+          ++cnt;
+#pragma unroll
+          for (int r = 0; r < R; ++r) thr[r] += 1;
+        }
+        bool p[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) p[r] = __double2hiint(P[(r + ph) & (R - 1)]) >= thr[r];
+#pragma unroll
+        for (int ww = 1; ww < R; ww <<= 1)
+#pragma unroll
+          for (int r = 0; r + ww < R; r += 2 * ww) p[r] = p[r] | p[r + ww];
+        pend = vote_any(p[0]);
+      } else if (VAR & 2) {
+        bool p[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) p[r] = __double2hiint(P[(r + ph) & (R - 1)]) >= thr[r];
+#pragma unroll
+        for (int ww = 1; ww < R; ww <<= 1)
+#pragma unroll
+          for (int r = 0; r + ww < R; r += 2 * ww) p[r] = p[r] | p[r + ww];
+        if (vote_any(p[0])) {
+          ++cnt;
+#pragma unroll
+          for (int r = 0; r < R; ++r) thr[r] += 1;
+        }
+      }
+    }
+  }
+  double acc = 0;
+  for (int r = 0; r < R; ++r) acc += P[r];
+  if (acc == 1234.5) out[0] = acc;
+  if (cnt) atomicAdd(hits, cnt);
+}
+
+template <int VAR>
+void run(const char* name, int blocks_per_sm) {
+  int dev = 0, nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  double* out; int* hits;
+  cudaMalloc(&out, 64); cudaMalloc(&hits, 4); cudaMemset(hits, 0, 4);
+  const int steps = 1 << 14;
+  const int grid = nsm * blocks_per_sm;
+  k<VAR><<<grid, 64>>>(out, steps, hits);
+  cudaDeviceSynchronize();
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  cudaEventRecord(a);
+  k<VAR><<<grid, 64>>>(out, steps, hits);
+  cudaEventRecord(b); cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  const double cells = (double)grid * 64 * R * steps;
+  int h; cudaMemcpy(&h, hits, 4, cudaMemcpyDeviceToHost);
+  printf("%-34s warps/SM=%2d  %.3f Tcell/s  (%.1f%% of 17T DFMA/2)  hits=%d %s\n", name, 2 * blocks_per_sm,
+         cells / ms / 1e9, cells / ms / 1e9 / 8.5 * 100, h, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  for (int bps : {8}) {
+    run<0>("dfma only", bps);
+    run<1>("+shfl/select", bps);
+    run<2>("+test/vote (no shfl)", bps);
+    run<3>("+shfl +test/vote", bps);
+    run<7>("+shfl +test/vote +smem", bps);
+    run<13>("+shfl +DEFERRED vote +smem", bps);
+    run<16>("3-op dfma only", bps);
+    run<23>("3-op +shfl +test/vote +smem", bps);
+  }
+  return 0;
+}
