@@ -47,6 +47,9 @@ constexpr int T = 128;    // head staging chunk (samples)
 #ifndef TSD_JOIN_MINB
 #define TSD_JOIN_MINB 8  // 8 CTAs x 2 warps per SM: caps registers at 128
 #endif
+#ifndef TSD_JOIN_MINB32
+#define TSD_JOIN_MINB32 8
+#endif
 
 template <int R>
 __host__ __device__ constexpr int padidx(int i) {
@@ -389,8 +392,220 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   __syncwarp();
 }
 
-template <int R, bool SELF>
-__global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join_f64(const JoinArgs a) {
+// ===========================================================================
+// FP32 mode: the same sweep with the normalised recurrence in packed
+// fma.rn.f32x2 / mul.rn.f32x2 (FFMA2: two slots per instruction). Window
+// statistics, heads and top edges stay FP64 and are rounded once; diagonals
+// restart from an FP64 head at every segment start and every task top, and
+// tasks are capped at 4096 rows, which bounds the FP32 drift.
+// Slot values live in 4 register pairs by physical index; because the slot
+// -> physical map rotates by one per step, the row data is kept in two
+// pairings: A = {(0,1),(2,3),(4,5),(6,7)} (even phase), B = {(1,2),(3,4),
+// (5,6),(7,0)} (odd phase).
+// ===========================================================================
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 pack2(float lo, float hi) {
+  return ((u64)__float_as_uint(hi) << 32) | (u64)__float_as_uint(lo);
+}
+__device__ __forceinline__ float lo2(u64 v) { return __uint_as_float((unsigned)v); }
+__device__ __forceinline__ float hi2(u64 v) { return __uint_as_float((unsigned)(v >> 32)); }
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) {
+  u64 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) {
+  u64 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float shfl_up1f(float v) {
+  asm volatile("shfl.sync.up.b32 %0, %0, 1, 0, -1;\n" : "+f"(v));
+  return v;
+}
+
+// FP32 column data, one 32-byte slot per column: {dg_b*s, dg_b*s, df_b*s,
+// df_b*s, s_k/s_{k-1}, s_k/s_{k-1}, invn_b/s, 0} (pairs pre-duplicated for f32x2)
+struct __align__(16) Col32 {
+  u64 dg2, df2, rk2;
+  float kf, pad;
+};
+static_assert(sizeof(Col32) == 32, "Col32 must match the double4 column slot");
+
+__device__ __forceinline__ int slot_thr32(float bK) { return bK > 0.0f ? __float_as_int(bK) : INT_MIN; }
+
+struct StepIn32 {
+  u64 dg2, df2, rk2;
+  float e, in;
+};
+
+__device__ __forceinline__ void prefetch32(const Col32* cb, const float* ep, float v7, StepIn32& d) {
+  const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(cb);
+  d.dg2 = a.x;
+  d.df2 = a.y;
+  d.rk2 = cb->rk2;
+  d.e = *ep;
+  d.in = shfl_up1f(v7);
+}
+
+struct SweepState32 {
+  u64 Q[4];       // slot values by physical index (pairs)
+  float bK[8];    // best K per slot
+  int thr[8];
+  StepIn32 nx;
+};
+
+__device__ __forceinline__ float qget(const u64 (&Q)[4], int q) { return (q & 1) ? hi2(Q[q >> 1]) : lo2(Q[q >> 1]); }
+__device__ __forceinline__ void qset(u64 (&Q)[4], int q, float v) {
+  Q[q >> 1] = (q & 1) ? pack2(lo2(Q[q >> 1]), v) : pack2(v, hi2(Q[q >> 1]));
+}
+
+__device__ __forceinline__ bool vote_any8f(const u64 (&Q)[4], int ph, const int (&thr)[8]) {
+  int h[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) h[(q - ph + 8) & 7] = __float_as_int(qget(Q, q));  // slot order
+  unsigned r;
+  asm volatile(
+      "{\n .reg .pred a, b;\n"
+      " setp.ge.s32 a, %1, %9;\n setp.ge.s32 b, %5, %13;\n"
+      " setp.ge.or.s32 a, %2, %10, a;\n setp.ge.or.s32 b, %6, %14, b;\n"
+      " setp.ge.or.s32 a, %3, %11, a;\n setp.ge.or.s32 b, %7, %15, b;\n"
+      " setp.ge.or.s32 a, %4, %12, a;\n setp.ge.or.s32 b, %8, %16, b;\n"
+      " or.pred a, a, b;\n vote.sync.any.pred a, a, -1;\n selp.u32 %0, 1, 0, a;\n}\n"
+      : "=r"(r)
+      : "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]), "r"(thr[0]),
+        "r"(thr[1]), "r"(thr[2]), "r"(thr[3]), "r"(thr[4]), "r"(thr[5]), "r"(thr[6]), "r"(thr[7]));
+  return r != 0;
+}
+
+template <int R>
+__device__ __forceinline__ void issue_chunk32(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int c) {
+  const double4* src = cx.colg + 32 * c + lane;
+  double4* dst = &sm.colbuf[c % 3][lane];
+  cp16(dst, src);
+  cp16(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16);
+  float* ring = reinterpret_cast<float*>(sm.ering);
+  const float* E = reinterpret_cast<const float*>(cx.E);
+  if (lane < 8) cp16(&ring[(c % 3) * 32 + 4 * lane], E + 32 * c + 4 * lane);
+  cp_commit();
+}
+
+template <int R>
+__device__ __forceinline__ void flush_block32(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int b) {
+  const int j = 32 * b + lane;
+  if (j < cx.ncol - 1) reinterpret_cast<float*>(cx.E)[j] = reinterpret_cast<const float*>(sm.ering)[(b % 3) * 32 + lane];
+}
+
+template <bool SELF, bool FIRST, bool GUARD>
+__device__ __forceinline__ void sweep_block32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, int k0, SweepState32& S,
+                                              const u64 (&FA)[4], const u64 (&GA)[4], const u64 (&FB)[4],
+                                              const u64 (&GB)[4], float* sbase, bool l0) {
+  constexpr int R = 8;
+  const int n = cx.ncol;
+  const Col32* ccur = reinterpret_cast<const Col32*>(&sm.colbuf[(k0 >> 5) % 3][k0 & 31]);
+  const Col32* cnext = reinterpret_cast<const Col32*>(&sm.colbuf[((k0 + R) >> 5) % 3][(k0 + R) & 31]);
+  const float* ring = reinterpret_cast<const float*>(sm.ering);
+  const int ebase = k0 % 96;
+  float* const st_prev = sbase + (k0 + 95) % 96;
+  float* const st_cur = sbase + ebase;
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const int k = k0 + u;
+    if (GUARD && k >= n) break;
+    const int ph = (R - u) & (R - 1);
+    if (!(FIRST && u == 0)) {
+      const float out = qget(S.Q, ph);
+      (u == 0 ? st_prev : st_cur + u - 1)[0] = out;
+      qset(S.Q, ph, l0 ? S.nx.e : S.nx.in);
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        // row pair of physical pair p at this phase (A for even, B for odd)
+        const u64 fa = (ph & 1) ? FB[(p - (ph + 1) / 2 + 4) & 3] : FA[(p - ph / 2 + 4) & 3];
+        const u64 ga = (ph & 1) ? GB[(p - (ph + 1) / 2 + 4) & 3] : GA[(p - ph / 2 + 4) & 3];
+        const u64 t = fma2(fa, S.nx.dg2, mul2(ga, S.nx.df2));
+        S.Q[p] = fma2(S.Q[p], S.nx.rk2, t);
+      }
+    }
+    if (!GUARD || k + 1 < n) prefetch32(u + 1 < R ? ccur + u + 1 : cnext, &ring[ebase + u], qget(S.Q, (ph + 7) & 7), S.nx);
+    if (vote_any8f(S.Q, ph, S.thr)) [[unlikely]] {
+      const float kf = (ccur + u)->kf;
+      const int col = cx.colbase + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float K = qget(S.Q, (r + ph) & 7) * kf;
+        bool ok = K > S.bK[r];
+        if (SELF) {
+          const long long d = cx.row0 + r - col;
+          ok = ok && (d > cx.excl || d < -cx.excl);
+        }
+        if (ok) {
+          S.bK[r] = K;
+          sm.bj[r][lane] = col;
+          S.thr[r] = slot_thr32(K);
+        }
+      }
+    }
+  }
+}
+
+template <bool SELF>
+__device__ void sweep_segment32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, const u64 (&FA)[4],
+                                const u64 (&GA)[4], const u64 (&FB)[4], const u64 (&GB)[4], SweepState32& S) {
+  constexpr int R = 8;
+  const int n = cx.ncol;
+  const int nchunks = (n + 31) >> 5;
+  float* const sbase = reinterpret_cast<float*>(lane == 31 ? sm.ering : sm.edummy);
+  const bool l0 = lane == 0;
+  __syncwarp();
+  issue_chunk32(sm, cx, lane, 0);
+  if (nchunks > 1) issue_chunk32(sm, cx, lane, 1); else cp_commit();
+  cp_wait<1>();
+  __syncwarp();
+  int flushed = 0;
+  if (n > 1)
+    prefetch32(reinterpret_cast<const Col32*>(&sm.colbuf[0][1]), reinterpret_cast<const float*>(sm.ering),
+               qget(S.Q, 7), S.nx);
+  auto chunk_turn = [&](int k0) {
+    if (((k0 + R) & 31) == 0 && k0 + R < n) {
+      const int c = (k0 + R) >> 5;
+      __syncwarp();
+      if (c >= 2 && cx.write_out) {
+        flush_block32(sm, cx, lane, c - 2);
+        flushed = c - 1;
+      }
+      __syncwarp();
+      if (c + 1 < nchunks) issue_chunk32(sm, cx, lane, c + 1); else cp_commit();
+      cp_wait<1>();
+      __syncwarp();
+    }
+  };
+  if (n <= R) {
+    sweep_block32<SELF, true, true>(sm, cx, lane, 0, S, FA, GA, FB, GB, sbase, l0);
+  } else {
+    chunk_turn(0);
+    sweep_block32<SELF, true, false>(sm, cx, lane, 0, S, FA, GA, FB, GB, sbase, l0);
+    int k0 = R;
+    for (; k0 + R <= n; k0 += R) {
+      chunk_turn(k0);
+      sweep_block32<SELF, false, false>(sm, cx, lane, k0, S, FA, GA, FB, GB, sbase, l0);
+    }
+    if (k0 < n) {
+      chunk_turn(k0);
+      sweep_block32<SELF, false, true>(sm, cx, lane, k0, S, FA, GA, FB, GB, sbase, l0);
+    }
+  }
+  cp_wait<0>();
+  __syncwarp();
+  if (cx.write_out) {
+    const int last = (n - 2) >> 5;
+    for (int b = flushed; b <= last && n >= 2; ++b) flush_block32(sm, cx, lane, b);
+  }
+  __syncwarp();
+}
+
+template <int R, bool SELF, bool F32>
+__global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_MINB) k_join(const JoinArgs a) {
   constexpr int H = Geo<R>::H;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem<R>* smem = reinterpret_cast<WarpSmem<R>*>(smem_raw);
@@ -445,14 +660,19 @@ __global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join
               // stored in the scale of column q - delta: the consumer multiplies
               // by s_{k}/s_{k-1} (delta = 1: row 0 adds nothing, so c~(0,q) =
               // E[q-1] * s_q / s_{q-1} must hold)
-              if (q < sg.ncol - 1 + delta)
-                cx.E[q - delta] = (out[r] - (a.mub[sg.col0 + q] - cS) * eU) * a.scale[sg.col0 + q - delta];
+              if (q < sg.ncol - 1 + delta) {
+                const double v = (out[r] - (a.mub[sg.col0 + q] - cS) * eU) * a.scale[sg.col0 + q - delta];
+                if constexpr (F32)
+                  reinterpret_cast<float*>(cx.E)[q - delta] = (float)v;
+                else
+                  cx.E[q - delta] = v;
+              }
             }
           }
           __threadfence_block();
           __syncwarp();
         }
-        SweepState<R> S;
+        double head[R];
         {  // left edge: cov(i, col0) for the band's rows
           double out[R];
 #ifdef TSD_ABL_NOHEADS
@@ -466,24 +686,60 @@ __global__ void __launch_bounds__(32 * WARPS, R == 8 ? TSD_JOIN_MINB : 4) k_join
           for (int r = 0; r < R; ++r) {
             const int64_t i = i0 + R * lane + r;
             const double mu = i < a.nrows ? a.mua[i] : cA;
-            S.P[r] = (out[r] - (mu - cA) * e) * s0;
+            head[r] = (out[r] - (mu - cA) * e) * s0;
           }
         }
-        // row data and row bests (reloaded per segment so they are not live
-        // across the heads)
-        double dfa[R], dga[R];
+        if constexpr (F32) {
+          // row data in both pairings, rounded once
+          float fa[R], ga[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int64_t i = i0 + R * lane + r;
-          const bool in = i < a.nrows;
-          dfa[r] = in ? a.dfa[i] : 0.0;
-          dga[r] = in ? a.dga[i] : 0.0;
-          S.bK[r] = sm.bK[r][lane];
-          S.thr[r] = slot_thr(S.bK[r]);
+          for (int r = 0; r < R; ++r) {
+            const int64_t i = i0 + R * lane + r;
+            const bool in = i < a.nrows;
+            fa[r] = in ? (float)a.dfa[i] : 0.0f;
+            ga[r] = in ? (float)a.dga[i] : 0.0f;
+          }
+          u64 FA[4], GA[4], FB[4], GB[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            FA[j] = pack2(fa[2 * j], fa[2 * j + 1]);
+            GA[j] = pack2(ga[2 * j], ga[2 * j + 1]);
+            FB[j] = pack2(fa[2 * j + 1], fa[(2 * j + 2) & 7]);
+            GB[j] = pack2(ga[2 * j + 1], ga[(2 * j + 2) & 7]);
+          }
+          SweepState32 S;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) S.Q[j] = pack2((float)head[2 * j], (float)head[2 * j + 1]);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const double bk = sm.bK[r][lane];
+            S.bK[r] = (float)bk;
+            S.thr[r] = isinf(bk) && bk > 0 ? INT_MAX : slot_thr32(S.bK[r]);
+          }
+          sweep_segment32<SELF>(sm, cx, lane, FA, GA, FB, GB, S);
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if (!(isinf(sm.bK[r][lane]) && sm.bK[r][lane] > 0)) sm.bK[r][lane] = (double)S.bK[r];
+        } else {
+          SweepState<R> S;
+#pragma unroll
+          for (int r = 0; r < R; ++r) S.P[r] = head[r];
+          // row data and row bests (reloaded per segment so they are not live
+          // across the heads)
+          double dfa[R], dga[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int64_t i = i0 + R * lane + r;
+            const bool in = i < a.nrows;
+            dfa[r] = in ? a.dfa[i] : 0.0;
+            dga[r] = in ? a.dga[i] : 0.0;
+            S.bK[r] = sm.bK[r][lane];
+            S.thr[r] = slot_thr(S.bK[r]);
+          }
+          sweep_segment<R, SELF>(sm, cx, lane, dfa, dga, S);
+#pragma unroll
+          for (int r = 0; r < R; ++r) sm.bK[r][lane] = S.bK[r];
         }
-        sweep_segment<R, SELF>(sm, cx, lane, dfa, dga, S);
-#pragma unroll
-        for (int r = 0; r < R; ++r) sm.bK[r][lane] = S.bK[r];
       }
       // band results: c = clamp(K * invn_a) (profiles.hpp:331, :335)
       double* oc = a.out_c + (int64_t)g * a.nrows;
@@ -542,6 +798,33 @@ __global__ void k_pack_cols(const double* __restrict__ df, const double* __restr
   const double sp = ivp > 0.0 ? ivp : 1.0;
   col[i] = make_double4(df[i] * sj, dg[i] * sj, sj / sp, iv > 0.0 ? 1.0 : 0.0);
   scale[i] = sj;
+}
+
+// FP32 column data (Col32 layout in the same 32-byte slots), from FP64 values
+__global__ void k_pack_cols32(const double* __restrict__ df, const double* __restrict__ dg,
+                              const double* __restrict__ invn, int64_t n, double4* __restrict__ col,
+                              double* __restrict__ scale) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n + 64) return;
+  Col32 c;
+  if (i >= n) {
+    c.dg2 = c.df2 = 0;
+    c.rk2 = pack2(1.0f, 1.0f);
+    c.kf = 0.0f;
+  } else {
+    const double iv = invn[i];
+    const double sj = iv > 0.0 ? iv : 1.0;
+    const double ivp = i > 0 ? invn[i - 1] : 0.0;
+    const double sp = ivp > 0.0 ? ivp : 1.0;
+    const float g = (float)(dg[i] * sj), f = (float)(df[i] * sj), r = (float)(sj / sp);
+    c.dg2 = pack2(g, g);
+    c.df2 = pack2(f, f);
+    c.rk2 = pack2(r, r);
+    c.kf = iv > 0.0 ? 1.0f : 0.0f;
+    scale[i] = sj;
+  }
+  c.pad = 0.0f;
+  reinterpret_cast<Col32*>(col)[i] = c;
 }
 
 __global__ void k_btil(const double* __restrict__ xb, const double* __restrict__ mub, const SegDev* __restrict__ segs,
@@ -674,7 +957,7 @@ __global__ void k_epilogue(const double* __restrict__ bc, const int64_t* __restr
 
 namespace {
 
-template <int R, bool SELF>
+template <int R, bool SELF, bool F32>
 int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st, Error* err,
                 int* launches) {
   constexpr int H = Geo<R>::H;
@@ -685,7 +968,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem_bytes = sizeof(WarpSmem<R>) * WARPS;
-  auto kern = k_join_f64<R, SELF>;
+  auto kern = k_join<R, SELF, F32>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * WARPS, smem_bytes);
@@ -727,7 +1010,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       }
       const double band = (double)H * (3.0 * cmax + (double)smax * (m + 64)) + 24.0 * cmax;
       const double top = (double)cmax * m;
-      const int bmax = std::min(nbands, 4096);
+      const int bmax = std::min(nbands, F32 ? 4096 / H : 4096);
       for (int b = 1; b <= bmax; ++b) {
         const int64_t nt = (int64_t)((nbands + b - 1) / b) * g;
         const int64_t waves = (nt + nwarps - 1) / nwarps;
@@ -780,8 +1063,12 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   CUDA_TRY(cudaMemcpyAsync(d_eoff, eoff.data(), sizeof(int) * nseg, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(d_gs, group_seg.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice, st));
   int nl = 0;
-  k_pack_cols<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(in.cols.df, in.cols.dg, in.cols.invn,
-                                                                          in.cols.nwin, d_col, d_scale);
+  if (F32)
+    k_pack_cols32<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(in.cols.df, in.cols.dg, in.cols.invn,
+                                                                              in.cols.nwin, d_col, d_scale);
+  else
+    k_pack_cols<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(in.cols.df, in.cols.dg, in.cols.invn,
+                                                                            in.cols.nwin, d_col, d_scale);
   ++nl;
   k_btil<<<nseg, 128, 0, st>>>(in.xb, in.cols.mu, d_segs, m, d_btil, d_ebt);
   ++nl;
@@ -851,13 +1138,12 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
 
 int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st, Error* err,
              int* launches) {
-  if (in.precision != 0) {
-    if (err) *err = Error{kInvalidArgument, "fp32 precision mode is not built in this version"};
-    return kInvalidArgument;
-  }
   const bool self = in.excl >= 0;
-  return self ? launch_join<8, true>(in, d_best_c, d_best_j, arena, st, err, launches)
-              : launch_join<8, false>(in, d_best_c, d_best_j, arena, st, err, launches);
+  if (in.precision == 1)
+    return self ? launch_join<8, true, true>(in, d_best_c, d_best_j, arena, st, err, launches)
+                : launch_join<8, false, true>(in, d_best_c, d_best_j, arena, st, err, launches);
+  return self ? launch_join<8, true, false>(in, d_best_c, d_best_j, arena, st, err, launches)
+              : launch_join<8, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
 }
 
 int run_epilogue(const double* d_best_c, const int64_t* d_best_j, const uint8_t* d_row_flag, int64_t nrows,

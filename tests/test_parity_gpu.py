@@ -281,3 +281,36 @@ def test_cpp_dropin_headers():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "[FAIL]" not in r.stdout
+
+
+# ------------------------------------------------------------- FP32 mode (north star: 1e-3 absolute)
+@pytest.mark.parametrize("m", [64, 200, 512])
+def test_fp32_mode_ab_and_dict(m):
+    """FP32 recurrence (FP64 stats, heads and top edges; diagonals restart at
+    least every 4096 rows): |d - d_ref| <= 1e-3 and the chosen index's exact
+    distance within 1e-3 of the reference minimum"""
+    q = synth.walk(30 + m, 40000)
+    segs = list(synth.walks(31 + m, 12, 1024))
+    starts = [2048 * s for s in range(12)]
+    P = tsd.join_dictionary(q, _dict(segs, starts, m), m, precision="fp32")
+    rv, ri = O.dict_join(q, segs, starts, m)
+    st = check_profile(P.values, P.indices, rv, ri, m, dict_dist(q, segs, starts, m), fp32=True, label=f"fp32 m={m}")
+    assert st["max_abs"] <= 1e-3
+    a, b = synth.walk(40, 6000), synth.walk(41, 30000)  # long single segment: many bands per diagonal
+    P = tsd.ab_join(a, b, m, precision="fp32")
+    rv, ri = O.ab_join(a, b, m)
+    check_profile(P.values, P.indices, rv, ri, m, ab_dist(a, b, m), fp32=True, label=f"fp32 ab m={m}")
+
+
+def test_fp32_mode_self_join_and_flat():
+    t, _ = synth.ecg(2, 12000)
+    P = tsd.self_join(t, 250, excl=62, precision="fp32")
+    rv, ri = O.self_join(t, 250, 62)
+    check_profile(P.values, P.indices, rv, ri, 250, ab_dist(t, t, 250), fp32=True, label="fp32 self")
+    a = synth.Rng(9).noise(2000)
+    a[300:500] = 2.5
+    b = synth.Rng(10).noise(1500)
+    b[700:800] = -1.0
+    P = tsd.ab_join(a, b, 64, precision="fp32")
+    rv, ri = O.ab_join(a, b, 64)
+    check_profile(P.values, P.indices, rv, ri, 64, ab_dist(a, b, 64), fp32=True, label="fp32 flat")

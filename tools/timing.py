@@ -11,7 +11,7 @@ for c in cfgs:
     nq, nseg, L, m = (int(x) for x in c.split(":"))
     q = synth.walk(4, nq); segs = synth.walks(5, nseg, L)
     D = t.Dictionary([t.Segment(L * s, segs[s]) for s in range(nseg)], m=m, source_length=nseg * L)
-    plan = t.DictPlan(D, m)
+    plan = t.DictPlan(D, m, os.environ.get("PREC", "fp64"))
     dq = torch.from_numpy(q).cuda(); cnt = nq - m + 1
     dv = torch.empty(cnt, dtype=torch.float64, device="cuda"); di = torch.empty(cnt, dtype=torch.int64, device="cuda")
     best = 1e9
