@@ -263,13 +263,16 @@ struct SweepState {
 // k0+R-1] are contiguous, only E[k0-1] may sit in the previous ring block,
 // and only step k0+R's column data in the next chunk.
 template <int R, bool SELF, bool FIRST, bool GUARD>
-__device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int k0, SweepState<R>& S,
-                                            const double (&dfa)[R], const double (&dga)[R], double* sbase, bool l0) {
+__device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int k0, int m96,
+                                            SweepState<R>& S, const double (&dfa)[R], const double (&dga)[R],
+                                            double* sbase, bool l0) {
+  // colbuf and the edge ring are both 96-entry rings indexed by column mod 96
   const int n = cx.ncol;
-  const double4* ccur = &sm.colbuf[(k0 >> 5) % 3][k0 & 31];
-  const double4* cnext = &sm.colbuf[((k0 + R) >> 5) % 3][(k0 + R) & 31];
-  const int ebase = k0 % 96;                       // ring position of E[k0]
-  double* const st_prev = sbase + (k0 + 95) % 96;  // E[k0-1]
+  const double4* cflat = &sm.colbuf[0][0];
+  const double4* ccur = cflat + m96;
+  const double4* cnext = cflat + (m96 + R == 96 ? 0 : m96 + R);
+  const int ebase = m96;                                    // ring position of E[k0]
+  double* const st_prev = sbase + (m96 == 0 ? 95 : m96 - 1);  // E[k0-1]
   double* const st_cur = sbase + ebase;
 #pragma unroll
   for (int u = 0; u < R; ++u) {
@@ -346,38 +349,37 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   __syncwarp();
   int flushed = 0;  // edge blocks [0, flushed) written back
   S.nx.kf = sm.colbuf[0][0].w;  // step 0 (heads) only needs the flat factor
-  auto chunk_turn = [&](int k0) {
-    // the block after this one opens chunk c: make it resident, retire edge
-    // block c-2, start loading chunk c+1 (3-deep rings keep in-use slots intact)
-    if (((k0 + R) & 31) == 0 && k0 + R < n) {
-      const int c = (k0 + R) >> 5;
-      __syncwarp();
-      if (c >= 2 && cx.write_out) {
-        flush_block(sm, cx, lane, c - 2);
-        flushed = c - 1;
-      }
-      __syncwarp();
-      if (c + 1 < nchunks) issue_chunk(sm, cx, lane, c + 1); else cp_commit();
+  // blocks of R steps; every 32 / R blocks the next block opens chunk c:
+  // make it resident, retire edge block c-2, start loading chunk c+1 (3-deep
+  // rings keep the in-use slots intact)
+  auto chunk_turn = [&](int c) {
+    __syncwarp();
+    if (c >= 2 && cx.write_out) {
+      flush_block(sm, cx, lane, c - 2);
+      flushed = c - 1;
+    }
+    __syncwarp();
+    if (c + 1 < nchunks) issue_chunk(sm, cx, lane, c + 1); else cp_commit();
 #ifndef TSD_ABL_NOWAIT
-      cp_wait<1>();
+    cp_wait<1>();
 #endif
-      __syncwarp();
-    }
+    __syncwarp();
   };
+  constexpr int BPC = 32 / R;  // blocks per chunk
   if (n <= R) {
-    sweep_block<R, SELF, true, true>(sm, cx, lane, 0, S, dfa, dga, sbase, l0);
+    sweep_block<R, SELF, true, true>(sm, cx, lane, 0, 0, S, dfa, dga, sbase, l0);
   } else {
-    chunk_turn(0);
-    sweep_block<R, SELF, true, false>(sm, cx, lane, 0, S, dfa, dga, sbase, l0);
-    int k0 = R;
+    sweep_block<R, SELF, true, false>(sm, cx, lane, 0, 0, S, dfa, dga, sbase, l0);
+    // the turn happens before the LAST block of a chunk: that block's final
+    // step prefetches the first column of the next chunk
+    int k0 = R, m96 = R, bic = 1;  // column, column mod 96, block index inside the chunk
     for (; k0 + R <= n; k0 += R) {
-      chunk_turn(k0);
-      sweep_block<R, SELF, false, false>(sm, cx, lane, k0, S, dfa, dga, sbase, l0);
+      if (bic == BPC - 1 && k0 + R < n) chunk_turn((k0 + R) >> 5);
+      sweep_block<R, SELF, false, false>(sm, cx, lane, k0, m96, S, dfa, dga, sbase, l0);
+      m96 = m96 + R == 96 ? 0 : m96 + R;
+      bic = bic == BPC - 1 ? 0 : bic + 1;
     }
-    if (k0 < n) {
-      chunk_turn(k0);
-      sweep_block<R, SELF, false, true>(sm, cx, lane, k0, S, dfa, dga, sbase, l0);
-    }
+    if (k0 < n) sweep_block<R, SELF, false, true>(sm, cx, lane, k0, m96, S, dfa, dga, sbase, l0);
   }
   cp_wait<0>();
   __syncwarp();
@@ -498,16 +500,17 @@ __device__ __forceinline__ void flush_block32(WarpSmem<R>& sm, const SweepCtx& c
 }
 
 template <bool SELF, bool FIRST, bool GUARD>
-__device__ __forceinline__ void sweep_block32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, int k0, SweepState32& S,
-                                              const u64 (&FA)[4], const u64 (&GA)[4], const u64 (&FB)[4],
-                                              const u64 (&GB)[4], float* sbase, bool l0) {
+__device__ __forceinline__ void sweep_block32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, int k0, int m96,
+                                              SweepState32& S, const u64 (&FA)[4], const u64 (&GA)[4],
+                                              const u64 (&FB)[4], const u64 (&GB)[4], float* sbase, bool l0) {
   constexpr int R = 8;
   const int n = cx.ncol;
-  const Col32* ccur = reinterpret_cast<const Col32*>(&sm.colbuf[(k0 >> 5) % 3][k0 & 31]);
-  const Col32* cnext = reinterpret_cast<const Col32*>(&sm.colbuf[((k0 + R) >> 5) % 3][(k0 + R) & 31]);
+  const Col32* cflat = reinterpret_cast<const Col32*>(&sm.colbuf[0][0]);
+  const Col32* ccur = cflat + m96;
+  const Col32* cnext = cflat + (m96 + R == 96 ? 0 : m96 + R);
   const float* ring = reinterpret_cast<const float*>(sm.ering);
-  const int ebase = k0 % 96;
-  float* const st_prev = sbase + (k0 + 95) % 96;
+  const int ebase = m96;
+  float* const st_prev = sbase + (m96 == 0 ? 95 : m96 - 1);
   float* const st_cur = sbase + ebase;
 #pragma unroll
   for (int u = 0; u < R; ++u) {
@@ -566,34 +569,30 @@ __device__ void sweep_segment32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, c
   if (n > 1)
     prefetch32(reinterpret_cast<const Col32*>(&sm.colbuf[0][1]), reinterpret_cast<const float*>(sm.ering),
                qget(S.Q, 7), S.nx);
-  auto chunk_turn = [&](int k0) {
-    if (((k0 + R) & 31) == 0 && k0 + R < n) {
-      const int c = (k0 + R) >> 5;
-      __syncwarp();
-      if (c >= 2 && cx.write_out) {
-        flush_block32(sm, cx, lane, c - 2);
-        flushed = c - 1;
-      }
-      __syncwarp();
-      if (c + 1 < nchunks) issue_chunk32(sm, cx, lane, c + 1); else cp_commit();
-      cp_wait<1>();
-      __syncwarp();
+  auto chunk_turn = [&](int c) {
+    __syncwarp();
+    if (c >= 2 && cx.write_out) {
+      flush_block32(sm, cx, lane, c - 2);
+      flushed = c - 1;
     }
+    __syncwarp();
+    if (c + 1 < nchunks) issue_chunk32(sm, cx, lane, c + 1); else cp_commit();
+    cp_wait<1>();
+    __syncwarp();
   };
+  constexpr int BPC = 32 / R;
   if (n <= R) {
-    sweep_block32<SELF, true, true>(sm, cx, lane, 0, S, FA, GA, FB, GB, sbase, l0);
+    sweep_block32<SELF, true, true>(sm, cx, lane, 0, 0, S, FA, GA, FB, GB, sbase, l0);
   } else {
-    chunk_turn(0);
-    sweep_block32<SELF, true, false>(sm, cx, lane, 0, S, FA, GA, FB, GB, sbase, l0);
-    int k0 = R;
+    sweep_block32<SELF, true, false>(sm, cx, lane, 0, 0, S, FA, GA, FB, GB, sbase, l0);
+    int k0 = R, m96 = R, bic = 1;
     for (; k0 + R <= n; k0 += R) {
-      chunk_turn(k0);
-      sweep_block32<SELF, false, false>(sm, cx, lane, k0, S, FA, GA, FB, GB, sbase, l0);
+      if (bic == BPC - 1 && k0 + R < n) chunk_turn((k0 + R) >> 5);
+      sweep_block32<SELF, false, false>(sm, cx, lane, k0, m96, S, FA, GA, FB, GB, sbase, l0);
+      m96 = m96 + R == 96 ? 0 : m96 + R;
+      bic = bic == BPC - 1 ? 0 : bic + 1;
     }
-    if (k0 < n) {
-      chunk_turn(k0);
-      sweep_block32<SELF, false, true>(sm, cx, lane, k0, S, FA, GA, FB, GB, sbase, l0);
-    }
+    if (k0 < n) sweep_block32<SELF, false, true>(sm, cx, lane, k0, m96, S, FA, GA, FB, GB, sbase, l0);
   }
   cp_wait<0>();
   __syncwarp();

@@ -90,8 +90,17 @@ __global__ void __launch_bounds__(64, 8) k(double* out, int steps, int* hits) {
           for (int r = 0; r + ww < R; r += 2 * ww) p[r] = p[r] | p[r + ww];
         if (vote_any(p[0])) {
           ++cnt;
+          if (VAR & 32) {  // big inline body (like the exact update), never taken
 #pragma unroll
-          for (int r = 0; r < R; ++r) thr[r] += 1;
+            for (int r = 0; r < R; ++r) {
+              const double K = P[(r + ph) & (R - 1)] * dgb;
+              if (K > (double)thr[r]) { thr[r] = __double2hiint(K) - 1; sm[w][r][lane] = K; }
+              if (K < -(double)thr[r]) { thr[r] = __double2hiint(K) + 1; sm[w][r][lane + 32] = K; }
+            }
+          } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) thr[r] += 1;
+          }
         }
       }
     }
@@ -131,7 +140,7 @@ int main() {
     run<3>("+shfl +test/vote", bps);
     run<7>("+shfl +test/vote +smem", bps);
     run<13>("+shfl +DEFERRED vote +smem", bps);
-    run<16>("3-op dfma only", bps);
+    run<7 | 32>("+shfl +test/vote +smem +BIG body", bps);
     run<23>("3-op +shfl +test/vote +smem", bps);
   }
   return 0;
