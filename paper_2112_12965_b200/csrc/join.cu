@@ -84,6 +84,8 @@ struct JoinArgs {
   const int* group_seg;  // [ngroups+1]
   int64_t ecap;          // per-warp edge capacity (doubles)
   double* edges;
+  double* hscr;   // per-warp head scratch [8][256]
+  int dmma_heads; // heads on the FP64 tensor cores (else register-blocked sliding dot)
   double* out_c;  // [ngroups][nrows]
   int64_t* out_j;
 };
@@ -195,6 +197,70 @@ __device__ void sliding_dot(WarpSmem<R>& sm, const double* __restrict__ Ug, doub
   }
 }
 
+// Left-edge heads of a band against a batch of up to 8 segments on the FP64
+// tensor cores (mma.sync.m8n8k4.f64): H[i][s] = sum_k xt[i + k] * btil_s[k],
+// a (256 x m) Toeplitz x (m x 8) product. The sweep is issue-bound, not
+// FP64-pipe-bound (profiles/), and one DMMA does the work of 8 DFMA warp
+// instructions. Output: hout[s * 256 + i] (per-warp global scratch), before
+// the (mu_i - cS) * e_s correction and the column scale.
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int R>
+__device__ __noinline__ void heads_dmma(WarpSmem<R>& sm, const double* __restrict__ Sg, int64_t s_avail, double cS,
+                                        const double* __restrict__ Bt, int nb, int m, int lane,
+                                        double* __restrict__ hout) {
+  static_assert(Geo<R>::H == 256, "heads_dmma tiles a 256-row band");
+  static_assert(Geo<R>::SLIDE >= 96 + 8 * 33, "heads_dmma stages in sm.slide");
+  const int g = lane >> 2, t = lane & 3;
+  double* xs = sm.slide;       // 96 staged query samples: rows [64 grp, +64) x k [k0, +32)
+  double* bs = sm.slide + 96;  // 8 segments x 32 k, row stride 33 (bank spread)
+  for (int grp = 0; grp < 4; ++grp) {
+    double c[8][2];
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) c[mt][0] = c[mt][1] = 0.0;
+    // register double buffer: chunk k0 + 32 is in flight while chunk k0 multiplies
+    double xr[3], br[8];
+    auto load = [&](int k0) {
+      const int kl = min(32, m - k0);
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int64_t gi = (int64_t)64 * grp + k0 + 32 * j + lane;
+        xr[j] = gi < s_avail ? Sg[gi] : cS;
+      }
+#pragma unroll
+      for (int sg = 0; sg < 8; ++sg) br[sg] = (sg < nb && lane < kl) ? Bt[(int64_t)sg * m + k0 + lane] : 0.0;
+    };
+    load(0);
+    for (int k0 = 0; k0 < m; k0 += 32) {
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < 3; ++j) xs[32 * j + lane] = xr[j] - cS;
+#pragma unroll
+      for (int sg = 0; sg < 8; ++sg) bs[sg * 33 + lane] = br[sg];
+      __syncwarp();
+      if (k0 + 32 < m) load(k0 + 32);
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const double bv = bs[g * 33 + 4 * ks + t];  // B[k = t][n = g]
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) dmma884(c[mt][0], c[mt][1], xs[8 * mt + g + 4 * ks + t], bv);
+      }
+    }
+    // C[row g][col 2t, 2t+1] of tile mt -> rows 64 grp + 8 mt + g, segments 2t, 2t+1
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const int row = 64 * grp + 8 * mt + g;
+      hout[(2 * t) * 256 + row] = c[mt][0];
+      hout[(2 * t + 1) * 256 + row] = c[mt][1];
+    }
+  }
+  __syncwarp();
+}
+
 struct SweepCtx {
   const double4* colg;  // global column data of this segment (col0 aligned)
   double* E;            // global edge array of this segment (j = 0 .. ncol-2)
@@ -224,13 +290,14 @@ __device__ __forceinline__ void flush_block(WarpSmem<R>& sm, const SweepCtx& cx,
   if (j < cx.ncol - 1) cx.E[j] = sm.ering[(b % 3) * 32 + lane];
 }
 
-// Test threshold of a slot: high word of its best K minus one (a candidate
-// can only win with hi(K) >= hi(bestK) - 1, so the integer test on K's high
-// word is conservative); bestK <= 0 passes everything (rare: no positive
-// candidate yet), inactive rows carry bestK = +inf and never pass.
+// Test threshold of a slot: the high word of its best K (for positive
+// doubles the bit pattern orders like the value, so K > bestK implies
+// hi(K) >= hi(bestK): the integer test is conservative); bestK <= 0 passes
+// everything (rare: no positive candidate yet), inactive rows carry
+// bestK = +inf and never pass.
 __device__ __forceinline__ int slot_thr(double bK) {
   const int h = __double2hiint(bK);
-  return h > 0 ? h - 1 : INT_MIN;
+  return h > 0 ? h : INT_MIN;
 }
 
 // Column data of one step: df_b * s, dg_b * s, s_k / s_{k-1}, and the factor
@@ -312,18 +379,20 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
       // exact update: strict K > bestK (columns arrive in increasing order,
       // so ties keep the lower column, profiles.hpp:70-77); flat column -> K = 0
       const int col = cx.colbase + k;
+      {
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const double K = S.P[(r + ph) & (R - 1)] * kf;
-        bool ok = K > S.bK[r] && (p[r] || kf == 0.0);
-        if (SELF) {
-          const long long d = cx.row0 + r - col;
-          ok = ok && (d > cx.excl || d < -cx.excl);  // profiles.hpp:281-284
-        }
-        if (ok) {
-          S.bK[r] = K;
-          sm.bj[r][lane] = col;
-          S.thr[r] = slot_thr(K);
+        for (int r = 0; r < R; ++r) {
+          const double K = S.P[(r + ph) & (R - 1)] * kf;
+          bool ok = K > S.bK[r] && (p[r] || kf == 0.0);
+          if (SELF) {
+            const long long d = cx.row0 + r - col;
+            ok = ok && (d > cx.excl || d < -cx.excl);  // profiles.hpp:281-284
+          }
+          if (ok) {
+            S.bK[r] = K;
+            sm.bj[r][lane] = col;
+            S.thr[r] = slot_thr(K);
+          }
         }
       }
     }
@@ -613,6 +682,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
   const int gw = blockIdx.x * WARPS + wl;
   const int nw = gridDim.x * WARPS;
   double* Ew = a.edges + (int64_t)gw * a.ecap;
+  double* Hw = a.hscr + (int64_t)gw * 2048;
   const int bpt = a.bands_per_task;
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 
@@ -672,14 +742,21 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           __syncwarp();
         }
         double head[R];
-        {  // left edge: cov(i, col0) for the band's rows
-          double out[R];
-#ifdef TSD_ABL_NOHEADS
-#pragma unroll
-          for (int r = 0; r < R; ++r) out[r] = 0.0;
+        {  // left edge: cov(i, col0) for the band's rows, batched 8 segments at a time
+#ifndef TSD_ABL_NOHEADS
+          if (((s - s_beg) & 7) == 0 && a.dmma_heads)
 #else
-          sliding_dot<R>(sm, a.btil + (int64_t)s * a.m, 0.0, a.xa + i0, a.na - i0, cA, a.m, lane, out, nullptr);
+          if (s == s_beg && b == b0)
 #endif
+            heads_dmma<R>(sm, a.xa + i0, a.na - i0, cA, a.btil + (int64_t)s * a.m, min(8, s_end - s), a.m, lane,
+                          Hw);
+          double out[R];
+          if (a.dmma_heads) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) out[r] = Hw[((s - s_beg) & 7) * 256 + R * lane + r];
+          } else {
+            sliding_dot<R>(sm, a.btil + (int64_t)s * a.m, 0.0, a.xa + i0, a.na - i0, cA, a.m, lane, out, nullptr);
+          }
           const double e = a.ebt[s], s0 = a.scale[sg.col0];
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -1052,9 +1129,10 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   double* d_btil = (double*)arena.get(sizeof(double) * (int64_t)nseg * m);
   double* d_ebt = (double*)arena.get(sizeof(double) * nseg);
   double* d_edges = (double*)arena.get(sizeof(double) * ecap * used_warps);
+  double* d_hscr = (double*)arena.get(sizeof(double) * 2048 * used_warps);
   double* d_pc = G > 1 ? (double*)arena.get(sizeof(double) * nrows * G) : d_best_c;
   int64_t* d_pj = G > 1 ? (int64_t*)arena.get(sizeof(int64_t) * nrows * G) : d_best_j;
-  if (!d_segs || !d_eoff || !d_gs || !d_col || !d_scale || !d_btil || !d_ebt || !d_edges || !d_pc || !d_pj) {
+  if (!d_segs || !d_eoff || !d_gs || !d_col || !d_scale || !d_hscr || !d_btil || !d_ebt || !d_edges || !d_pc || !d_pj) {
     if (err) *err = Error{kCudaError, "device allocation failed for the join"};
     return kCudaError;
   }
@@ -1097,6 +1175,11 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   a.group_seg = d_gs;
   a.ecap = ecap;
   a.edges = d_edges;
+  a.hscr = d_hscr;
+  {
+    const char* e = getenv("TSD_DMMA_HEADS");
+    a.dmma_heads = e ? atoi(e) : 1;
+  }
   a.out_c = d_pc;
   a.out_j = d_pj;
 #ifdef TSD_COUNT_EXACT
