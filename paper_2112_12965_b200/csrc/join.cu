@@ -86,6 +86,8 @@ struct JoinArgs {
   double* edges;
   double* hscr;   // per-warp head scratch [8][256]
   int dmma_heads; // heads on the FP64 tensor cores (else register-blocked sliding dot)
+  const double* heads;  // precomputed final heads [seg][hstride] (heads_fft.cu), or null
+  int64_t hstride;
   double* out_c;  // [ngroups][nrows]
   int64_t* out_j;
 };
@@ -742,7 +744,15 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           __syncwarp();
         }
         double head[R];
-        {  // left edge: cov(i, col0) for the band's rows, batched 8 segments at a time
+        if (a.heads) {  // left edge precomputed by FFT correlation (heads_fft.cu)
+          const double2* hp = reinterpret_cast<const double2*>(a.heads + s * a.hstride + i0 + R * lane);
+#pragma unroll
+          for (int r = 0; r < R / 2; ++r) {
+            const double2 h2 = __ldg(hp + r);
+            head[2 * r] = h2.x;
+            head[2 * r + 1] = h2.y;
+          }
+        } else {  // left edge: cov(i, col0) for the band's rows, batched 8 segments at a time
 #ifndef TSD_ABL_NOHEADS
           if (((s - s_beg) & 7) == 0 && a.dmma_heads)
 #else
@@ -1149,6 +1159,24 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   ++nl;
   k_btil<<<nseg, 128, 0, st>>>(in.xb, in.cols.mu, d_segs, m, d_btil, d_ebt);
   ++nl;
+  // heads by FFT correlation when there are several segments and the
+  // [seg][row] array fits comfortably (C4: 256 x 2^24 doubles = 34 GB)
+  const int64_t hstride = (int64_t)nbands * H;
+  double* d_heads = nullptr;
+  {
+    const char* e = getenv("TSD_FFT_HEADS");
+    const bool want = (e ? atoi(e) != 0 : true) && nseg >= 2 && heads_fft_supported(m);
+    size_t fr = 0, tot = 0;
+    const size_t hbytes = sizeof(double) * (size_t)nseg * (size_t)hstride;
+    if (want && cudaMemGetInfo(&fr, &tot) == cudaSuccess && hbytes < fr / 2) {
+      d_heads = (double*)arena.get(hbytes);
+      if (d_heads) {
+        const int rc = compute_heads_fft(in.xa, in.na, nrows, hstride, in.rows.mu, d_btil, d_ebt, d_scale, d_segs,
+                                         nseg, m, d_heads, hstride, arena, st, &nl, err);
+        if (rc != kOk) return rc;
+      }
+    }
+  }
   JoinArgs a;
   a.xa = in.xa;
   a.na = in.na;
@@ -1180,6 +1208,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     const char* e = getenv("TSD_DMMA_HEADS");
     a.dmma_heads = e ? atoi(e) : 1;
   }
+  a.heads = d_heads;
+  a.hstride = hstride;
   a.out_c = d_pc;
   a.out_j = d_pj;
 #ifdef TSD_COUNT_EXACT

@@ -109,6 +109,16 @@ struct JoinInputs {
 int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st,
              Error* err, int* launches);
 
+// heads_fft.cu ---------------------------------------------------------------
+// Final left-edge heads of every (row, segment) by FFT correlation:
+// d_heads[s * hstride + i] for i < hrows. heads_fft_supported(m): m fits the
+// 4096-point transform with >= 512 rows per block.
+int heads_fft_supported(int m);
+int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrows, const double* d_mua,
+                      const double* d_btil, const double* d_ebt, const double* d_scale, const SegDev* d_segs,
+                      int nseg, int m, double* d_heads, int64_t hstride, Arena& arena, cudaStream_t st, int* launches,
+                      Error* err);
+
 // Epilogue: corr -> distance (series.hpp:153-161), concat column -> source
 // coordinate (dictionary.hpp:183-188), (inf, -1) sentinel for rows without an
 // admissible neighbour (profiles.hpp:149-151), row compaction for batched

@@ -174,6 +174,26 @@ def test_dict_join_C3_shape_reduced():
     check_profile(P.values, P.indices, rv, ri, m, dict_dist(q, segs, starts, m), label="C3 reduced")
 
 
+@pytest.mark.parametrize("m,nseg,L", [(512, 40, 1024), (100, 9, 700), (3585, 3, 4000), (3586, 2, 3700)])
+def test_fft_heads_vs_direct_heads_and_oracle(monkeypatch, m, nseg, L):
+    """Segment heads by FFT correlation (heads_fft.cu, the default for >= 2
+    segments) against the direct in-kernel heads (TSD_FFT_HEADS=0) and the
+    oracle; m = 3585 is the largest window the 4096-point transform takes,
+    m = 3586 falls back to the direct heads."""
+    q = synth.walk(31, 40000)
+    segs = list(synth.walks(32, nseg, L))
+    starts = [2 * L * s for s in range(nseg)]
+    D = _dict(segs, starts, m)
+    monkeypatch.setenv("TSD_FFT_HEADS", "1")
+    P = tsd.join_dictionary(q, D, m)
+    monkeypatch.setenv("TSD_FFT_HEADS", "0")
+    Pd = tsd.join_dictionary(q, D, m)
+    dd = dict_dist(q, segs, starts, m)
+    check_profile(P.values, P.indices, Pd.values, Pd.indices, m, dd, label=f"fft vs direct m={m}")
+    rv, ri = O.dict_join(q, segs, starts, m)
+    check_profile(P.values, P.indices, rv, ri, m, dd, label=f"fft vs oracle m={m}")
+
+
 def test_batched_C5_shape():
     """BASELINE C5 shape: transport-like series vs one shared 64 x 1024 dictionary,
     m = 128, one device pass; each series equals its own join_dictionary oracle"""
