@@ -702,6 +702,31 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
         sm.bK[r][lane] = f == 1 ? -kInf : kInf;  // valid non-flat rows take part; +inf never passes
         sm.bj[r][lane] = -1;
       }
+      if (!F32 && a.heads) {
+        // Seed each row's best with one ulp below its best head candidate
+        // (column 0 of every segment of the group, K = head * kf exactly as
+        // the sweep will compute it). That column is still visited and
+        // recorded by the strict test, and anything at least as good earlier
+        // in column order wins as before, so the (max, lowest index) result
+        // is unchanged -- but the running best no longer climbs from -inf in
+        // every band, which was most of the exact-update traffic.
+        double mk[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) mk[r] = -kInf;
+        for (int s = s_beg; s < s_end; ++s) {
+          const double kf0 = a.col[a.segs[s].col0].w;
+          const double2* hp = reinterpret_cast<const double2*>(a.heads + s * a.hstride + i0 + R * lane);
+#pragma unroll
+          for (int r = 0; r < R / 2; ++r) {
+            const double2 h2 = __ldg(hp + r);
+            mk[2 * r] = fmax(mk[2 * r], h2.x * kf0);
+            mk[2 * r + 1] = fmax(mk[2 * r + 1], h2.y * kf0);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (sm.bK[r][lane] == -kInf && mk[r] > -kInf) sm.bK[r][lane] = nextafter(mk[r], -kInf);
+      }
       const double cA = a.mua[i0];
       for (int s = s_beg; s < s_end; ++s) {
         const SegDev sg = a.segs[s];
