@@ -200,12 +200,23 @@ struct HeadsArgs {
   const double* ebt;    // sum of btil per segment
   const double* scale;  // column scale per concatenated column
   const SegDev* segs;
-  int nseg, npairs, m, Q, ppc;  // ppc: pairs per CTA
+  const double4* col;     // packed column data (.w = kf: 1, or 0 for a flat column)
+  const uint8_t* flag_a;  // row flags (bit0 valid, bit1 flat)
+  int nseg, npairs, m, Q;
   double* heads;
+  unsigned long long* seed;  // per row: order-preserving key of max_s head * kf (0 = none), or null
+  int ppc;                   // pairs per CTA
 };
+
+// order-preserving map double -> u64 (key(a) < key(b) iff a < b; 0 below all)
+__device__ __forceinline__ unsigned long long order_key(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
 
 __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
   extern __shared__ double2 fsm[];
+  double* mk = reinterpret_cast<double*>(fsm + FFT_PAD);  // per-row running max of head * kf
   const int j = threadIdx.x;
   const int64_t blk0 = (int64_t)blockIdx.x * a.Q;
   const int p0 = blockIdx.y * a.ppc, p1 = min(a.npairs, p0 + a.ppc);
@@ -215,15 +226,9 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
   for (int r = 0; r < 16; ++r) {
     const int64_t n = blk0 + j + 256 * r;
     X[r] = make_double2((n < a.na ? a.x[n] : c) - c, 0.0);
+    mk[j + 256 * r] = -INFINITY;
   }
   fft4096<false>(X, fsm, j, a.tw);
-  // this thread's rows and their centring corrections (reused by every pair)
-  double dmu[16];
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const int64_t i = blk0 + j + 256 * r;
-    dmu[r] = (i < a.nrows ? a.mua[i] : c) - c;
-  }
   const double invN = 1.0 / FFT_N;
   for (int p = p0; p < p1; ++p) {
     double2 v[16];
@@ -232,19 +237,37 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
     for (int r = 0; r < 16; ++r) v[r] = cmul(X[r], __ldg(&sp[j + 256 * r]));
     fft4096<true>(v, fsm, j, a.tw);
     const int s0 = 2 * p, s1 = 2 * p + 1;
-    const double e0 = a.ebt[s0], f0 = a.scale[a.segs[s0].col0];
+    const int64_t c0 = a.segs[s0].col0;
+    const double e0 = a.ebt[s0], f0 = a.scale[c0], k0 = a.col[c0].w;
     const bool two = s1 < a.nseg;
-    const double e1 = two ? a.ebt[s1] : 0.0, f1 = two ? a.scale[a.segs[s1].col0] : 0.0;
+    const int64_t c1 = two ? a.segs[s1].col0 : c0;
+    const double e1 = two ? a.ebt[s1] : 0.0, f1 = two ? a.scale[c1] : 0.0, k1 = two ? a.col[c1].w : 0.0;
     double* h0 = a.heads + (int64_t)s0 * a.hstride;
     double* h1 = a.heads + (int64_t)s1 * a.hstride;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const int q = j + 256 * r;
       const int64_t i = blk0 + q;
+      const double dmu = (i < a.nrows ? __ldg(&a.mua[i]) : c) - c;
       if (q < a.Q && i < a.hrows) {
-        h0[i] = (v[r].x * invN - dmu[r] * e0) * f0;
-        if (two) h1[i] = (v[r].y * invN - dmu[r] * e1) * f1;
+        const double g0 = (v[r].x * invN - dmu * e0) * f0;
+        h0[i] = g0;
+        double best = fmax(mk[q], g0 * k0);
+        if (two) {
+          const double g1 = (v[r].y * invN - dmu * e1) * f1;
+          h1[i] = g1;
+          best = fmax(best, g1 * k1);
+        }
+        mk[q] = best;
       }
+    }
+  }
+  if (a.seed) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int q = j + 256 * r;
+      const int64_t i = blk0 + q;
+      if (q < a.Q && i < a.nrows && mk[q] > -INFINITY) atomicMax(&a.seed[i], order_key(mk[q]));
     }
   }
 }
@@ -254,9 +277,9 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
 int heads_fft_supported(int m) { return m >= 1 && m <= FFT_N - 512 + 1; }
 
 int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrows, const double* d_mua,
-                      const double* d_btil, const double* d_ebt, const double* d_scale, const SegDev* d_segs,
-                      int nseg, int m, double* d_heads, int64_t hstride, Arena& arena, cudaStream_t st, int* launches,
-                      Error* err) {
+                      const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double* d_scale,
+                      const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
+                      unsigned long long* d_seed, Arena& arena, cudaStream_t st, int* launches, Error* err) {
   const int npairs = (nseg + 1) / 2;
   double2* d_tw = (double2*)arena.get(sizeof(double2) * FFT_N);
   double2* d_spec = (double2*)arena.get(sizeof(double2) * FFT_N * (size_t)npairs);
@@ -265,8 +288,9 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
     return kCudaError;
   }
   const size_t smem = sizeof(double2) * FFT_PAD;
+  const size_t smem_h = smem + sizeof(double) * FFT_N;
   CUDA_TRY(cudaFuncSetAttribute(k_pair_spectra, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  CUDA_TRY(cudaFuncSetAttribute(k_heads_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  CUDA_TRY(cudaFuncSetAttribute(k_heads_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h));
   k_fft_twiddles<<<FFT_N / 256, 256, 0, st>>>(d_tw);
   k_pair_spectra<<<npairs, FFT_T, smem, st>>>(d_btil, nseg, m, d_tw, d_spec);
   HeadsArgs a;
@@ -281,15 +305,19 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
   a.ebt = d_ebt;
   a.scale = d_scale;
   a.segs = d_segs;
+  a.col = d_col;
+  a.flag_a = d_flag_a;
   a.nseg = nseg;
   a.npairs = npairs;
   a.m = m;
   a.Q = ((FFT_N - m + 1) / 256) * 256;
-  a.ppc = 16;
   a.heads = d_heads;
+  a.seed = d_seed;
+  a.ppc = 16;
+  if (d_seed) CUDA_TRY(cudaMemsetAsync(d_seed, 0, sizeof(unsigned long long) * nrows, st));
   const int64_t nblk = (hrows + a.Q - 1) / a.Q;
   dim3 grid((unsigned)nblk, (unsigned)((npairs + a.ppc - 1) / a.ppc));
-  k_heads_fft<<<grid, FFT_T, smem, st>>>(a);
+  k_heads_fft<<<grid, FFT_T, smem_h, st>>>(a);
   CUDA_TRY(cudaGetLastError());
   if (launches) *launches += 3;
   return kOk;

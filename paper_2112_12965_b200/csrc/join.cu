@@ -88,6 +88,7 @@ struct JoinArgs {
   int dmma_heads; // heads on the FP64 tensor cores (else register-blocked sliding dot)
   const double* heads;  // precomputed final heads [seg][hstride] (heads_fft.cu), or null
   int64_t hstride;
+  const unsigned long long* seed;  // per-row order key of the best head candidate (heads_fft.cu), or null
   double* out_c;  // [ngroups][nrows]
   int64_t* out_j;
 };
@@ -702,30 +703,24 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
         sm.bK[r][lane] = f == 1 ? -kInf : kInf;  // valid non-flat rows take part; +inf never passes
         sm.bj[r][lane] = -1;
       }
-      if (!F32 && a.heads) {
-        // Seed each row's best with one ulp below its best head candidate
-        // (column 0 of every segment of the group, K = head * kf exactly as
-        // the sweep will compute it). That column is still visited and
-        // recorded by the strict test, and anything at least as good earlier
-        // in column order wins as before, so the (max, lowest index) result
-        // is unchanged -- but the running best no longer climbs from -inf in
-        // every band, which was most of the exact-update traffic.
-        double mk[R];
+      if (!F32 && a.seed) {
+        // Seed each row's best with its precomputed lower bound: one ulp below
+        // the best column-0 candidate over ALL segments (heads_fft.cu). The
+        // cell achieving it is visited by exactly one group and recorded by
+        // the strict test there; anything at least as good earlier in column
+        // order wins as before; a group holding nothing better leaves the row
+        // without a candidate (-1), which the group merge skips. The result is
+        // unchanged, but the running best no longer climbs from -inf in every
+        // band and group -- most of the exact-update traffic.
 #pragma unroll
-        for (int r = 0; r < R; ++r) mk[r] = -kInf;
-        for (int s = s_beg; s < s_end; ++s) {
-          const double kf0 = a.col[a.segs[s].col0].w;
-          const double2* hp = reinterpret_cast<const double2*>(a.heads + s * a.hstride + i0 + R * lane);
-#pragma unroll
-          for (int r = 0; r < R / 2; ++r) {
-            const double2 h2 = __ldg(hp + r);
-            mk[2 * r] = fmax(mk[2 * r], h2.x * kf0);
-            mk[2 * r + 1] = fmax(mk[2 * r + 1], h2.y * kf0);
+        for (int r = 0; r < R; ++r) {
+          const int64_t i = i0 + R * lane + r;
+          const unsigned long long key = sm.bK[r][lane] == -kInf ? a.seed[i] : 0ull;  // -inf: valid row
+          if (key != 0ull) {
+            const unsigned long long bits = (key >> 63) ? (key & 0x7fffffffffffffffull) : ~key;
+            sm.bK[r][lane] = nextafter(__longlong_as_double((long long)bits), -kInf);
           }
         }
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (sm.bK[r][lane] == -kInf && mk[r] > -kInf) sm.bK[r][lane] = nextafter(mk[r], -kInf);
       }
       const double cA = a.mua[i0];
       for (int s = s_beg; s < s_end; ++s) {
@@ -1188,6 +1183,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   // [seg][row] array fits comfortably (C4: 256 x 2^24 doubles = 34 GB)
   const int64_t hstride = (int64_t)nbands * H;
   double* d_heads = nullptr;
+  unsigned long long* d_seed = nullptr;
   {
     const char* e = getenv("TSD_FFT_HEADS");
     const bool want = (e ? atoi(e) != 0 : true) && nseg >= 2 && heads_fft_supported(m);
@@ -1195,9 +1191,11 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     const size_t hbytes = sizeof(double) * (size_t)nseg * (size_t)hstride;
     if (want && cudaMemGetInfo(&fr, &tot) == cudaSuccess && hbytes < fr / 2) {
       d_heads = (double*)arena.get(hbytes);
-      if (d_heads) {
-        const int rc = compute_heads_fft(in.xa, in.na, nrows, hstride, in.rows.mu, d_btil, d_ebt, d_scale, d_segs,
-                                         nseg, m, d_heads, hstride, arena, st, &nl, err);
+      d_seed = F32 ? nullptr : (unsigned long long*)arena.get(sizeof(unsigned long long) * nrows);
+      if (d_heads && (F32 || d_seed)) {
+        const int rc = compute_heads_fft(in.xa, in.na, nrows, hstride, in.rows.mu, in.rows.flag, d_btil, d_ebt,
+                                         d_scale, d_col, d_segs, nseg, m, d_heads, hstride, d_seed, arena, st, &nl,
+                                         err);
         if (rc != kOk) return rc;
       }
     }
@@ -1235,6 +1233,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   }
   a.heads = d_heads;
   a.hstride = hstride;
+  a.seed = d_heads ? d_seed : nullptr;
   a.out_c = d_pc;
   a.out_j = d_pj;
 #ifdef TSD_COUNT_EXACT

@@ -37,7 +37,14 @@ __global__ void __launch_bounds__(64, 8) k(double* out, int steps, int* hits) {
   double dfb = 0.5, dgb = 0.25, e = 1.0;
   int cnt = 0;
   bool pend = false;
+  double bKd[R];
+  for (int r = 0; r < R; ++r) bKd[r] = 1e300;
   for (int s = 0; s < steps; s += R) {
+    if (VAR & 64) {  // per-block threshold: thr = hi(bestK * min column norm of the block)
+      const double nmin = sm[w][s & 7][lane & 7] + 1.0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) thr[r] = __double2hiint(bKd[r] * nmin);
+    }
 #pragma unroll
     for (int u = 0; u < R; ++u) {
       const int ph = (R - u) & (R - 1);
@@ -142,6 +149,9 @@ int main() {
     run<13>("+shfl +DEFERRED vote +smem", bps);
     run<7 | 32>("+shfl +test/vote +smem +BIG body", bps);
     run<23>("3-op +shfl +test/vote +smem", bps);
+    run<29>("3-op +shfl +DEFERRED vote +smem", bps);
+    run<7 | 64>("2-op +blockthr +shfl +test/vote +smem", bps);
+    run<13 | 64>("2-op +blockthr +shfl +DEFERRED +smem", bps);
   }
   return 0;
 }
