@@ -2,10 +2,9 @@
 //
 // Every diagonal that enters segment s at its window 0 needs one m-term dot
 // product (window_dot, profiles.hpp:101-108):
-//   head(i, s) = cov(i, col0_s) * s0_s
-//              = (sum_k (x[i+k] - c) * btil_s[k] - (mu_i - c) * e_s) * s0_s
-// (btil_s = centred window 0 of segment s, e_s = sum btil_s, s0_s = the
-// column scale of col0_s, c any constant). Done directly that is m FMAs per
+//   head(i, s) = cov(i, col0_s)
+//              = sum_k (x[i+k] - c) * btil_s[k] - (mu_i - c) * e_s
+// (btil_s = centred window 0 of segment s, e_s = sum btil_s, c any constant). Done directly that is m FMAs per
 // (row, segment): for the headline config (m = 512, 1024-sample segments)
 // as many FP64 operations as a third of the sweep itself. As a correlation
 // of the query with btil_s it is O(log N) per output by FFT:
@@ -15,8 +14,8 @@
 //     z = btil_s + i btil_{s+1}, IFFT(X . Z[-f]) = corr(x, btil_s) +
 //     i corr(x, btil_{s+1}) (x real), Z precomputed per dictionary;
 //   * ~25 FP64 operations per head instead of 512 FMAs.
-// Output: heads[s * hstride + i] -- FINAL head values in the sweep's column
-// scale, read by k_join (join.cu) at the start of each (band, segment).
+// Output: heads[s * hstride + i], read by k_join (join.cu) at the start of
+// each (band, segment); the FP32 sweep scales them by its column scale.
 //
 // FFT: Stockham autosort, radix 16 x 3 passes, 256 threads, one 4096-point
 // transform per CTA in padded shared memory (pad(i) = i + i/16 keeps the
@@ -197,10 +196,9 @@ struct HeadsArgs {
   const double* mua;  // window means
   const double2* spec;
   const double2* tw;
-  const double* ebt;    // sum of btil per segment
-  const double* scale;  // column scale per concatenated column
+  const double* ebt;  // sum of btil per segment
   const SegDev* segs;
-  const double4* col;     // packed column data (.w = kf: 1, or 0 for a flat column)
+  const double4* col;     // FP64 packed column data (.z = invn_b), read for the seeds
   const uint8_t* flag_a;  // row flags (bit0 valid, bit1 flat)
   int nseg, npairs, m, Q;
   double* heads;
@@ -238,10 +236,10 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
     fft4096<true>(v, fsm, j, a.tw);
     const int s0 = 2 * p, s1 = 2 * p + 1;
     const int64_t c0 = a.segs[s0].col0;
-    const double e0 = a.ebt[s0], f0 = a.scale[c0], k0 = a.col[c0].w;
+    const double e0 = a.ebt[s0], k0 = a.seed ? a.col[c0].z : 0.0;
     const bool two = s1 < a.nseg;
     const int64_t c1 = two ? a.segs[s1].col0 : c0;
-    const double e1 = two ? a.ebt[s1] : 0.0, f1 = two ? a.scale[c1] : 0.0, k1 = two ? a.col[c1].w : 0.0;
+    const double e1 = two ? a.ebt[s1] : 0.0, k1 = (two && a.seed) ? a.col[c1].z : 0.0;
     double* h0 = a.heads + (int64_t)s0 * a.hstride;
     double* h1 = a.heads + (int64_t)s1 * a.hstride;
 #pragma unroll
@@ -250,11 +248,11 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
       const int64_t i = blk0 + q;
       const double dmu = (i < a.nrows ? __ldg(&a.mua[i]) : c) - c;
       if (q < a.Q && i < a.hrows) {
-        const double g0 = (v[r].x * invN - dmu * e0) * f0;
+        const double g0 = v[r].x * invN - dmu * e0;
         h0[i] = g0;
         double best = fmax(mk[q], g0 * k0);
         if (two) {
-          const double g1 = (v[r].y * invN - dmu * e1) * f1;
+          const double g1 = v[r].y * invN - dmu * e1;
           h1[i] = g1;
           best = fmax(best, g1 * k1);
         }
@@ -277,8 +275,7 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
 int heads_fft_supported(int m) { return m >= 1 && m <= FFT_N - 512 + 1; }
 
 int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrows, const double* d_mua,
-                      const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double* d_scale,
-                      const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
+                      const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
                       unsigned long long* d_seed, Arena& arena, cudaStream_t st, int* launches, Error* err) {
   const int npairs = (nseg + 1) / 2;
   double2* d_tw = (double2*)arena.get(sizeof(double2) * FFT_N);
@@ -303,7 +300,6 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
   a.spec = d_spec;
   a.tw = d_tw;
   a.ebt = d_ebt;
-  a.scale = d_scale;
   a.segs = d_segs;
   a.col = d_col;
   a.flag_a = d_flag_a;

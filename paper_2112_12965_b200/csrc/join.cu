@@ -31,6 +31,7 @@
 //     Flat rows (invn_a == 0) are resolved in the epilogue from the flat
 //     column table (profiles.hpp:332-336 gives them c in {0, 1}).
 #include <algorithm>
+#include <cfloat>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -72,8 +73,8 @@ struct JoinArgs {
   const uint8_t* flag_a;
   const double* xb;
   const double* mub;
-  const double4* col;   // normalised-recurrence column data (k_pack_cols), padded by 64
-  const double* scale;  // s_j per concatenated column
+  const double4* col;   // column data (k_pack_cols / k_pack_cols32), padded by 64
+  const double* scale;  // s_j per concatenated column (FP32 normalised recurrence)
   const SegDev* segs;
   const int* seg_eoff;  // compact edge offset of each segment inside its group (even)
   const double* btil;   // [nseg][m] centred samples of each segment's window 0
@@ -98,7 +99,7 @@ struct __align__(16) WarpSmem {
   double4 colbuf[3][32];
   double ering[96];
   double edummy[96];  // lanes 0..30 store here so lane 31's edge store needs no branch
-  double bK[R][32];  // best K = cov * invn_b per slot (row factor invn_a left out)
+  double bK[R][32];  // best K = cov * invn_b per slot (row factor invn_a left out); +inf = inactive row
   int bj[R][32];     // its concatenated column
   double slide[Geo<R>::SLIDE];
   double unif[T];
@@ -293,38 +294,45 @@ __device__ __forceinline__ void flush_block(WarpSmem<R>& sm, const SweepCtx& cx,
   if (j < cx.ncol - 1) cx.E[j] = sm.ering[(b % 3) * 32 + lane];
 }
 
-// Test threshold of a slot: the high word of its best K (for positive
-// doubles the bit pattern orders like the value, so K > bestK implies
-// hi(K) >= hi(bestK): the integer test is conservative); bestK <= 0 passes
-// everything (rare: no positive candidate yet), inactive rows carry
-// bestK = +inf and never pass.
-__device__ __forceinline__ int slot_thr(double bK) {
-  const int h = __double2hiint(bK);
-  return h > 0 ? h : INT_MIN;
-}
+// FP64 sweep: the unnormalised centred recurrence of the reference
+// (profiles.hpp:330), 2 FMAs per cell,
+//   cov(i, k) = cov(i-1, k-1) + df_a[i] dg_b[k] + dg_a[i] df_b[k],
+// and a row test without a per-cell multiply: the candidate K = cov * invn_b
+// (row factor invn_a left out) can beat bestK > 0 only if
+//   cov > bestK / invn_b >= bestK * nmin(block),
+// nmin = (1 - 2^-40) x the smallest window norm among the block's 8 columns
+// (k_pack_cols; the factor absorbs the roundings of the exact test). The
+// threshold is compared on high words (integer pipe): thr = hi(bestK+ * nmin)
+// with bestK+ = bestK if bestK > 0, else -0.0, whose product -0.0 has high
+// word INT_MIN (passes everything). Inactive rows carry bestK = +inf
+// (thr = hi(inf), never passed by a finite cov). A pass runs the exact update
+// K = cov * invn_b > bestK against the real bestK in shared memory.
+__device__ __forceinline__ double kplus(double bK) { return bK > 0.0 ? bK : -0.0; }
+#ifndef TSD_TB
+#define TSD_TB 4
+#endif
+constexpr int TB = TSD_TB;  // threshold block (columns); nmin spans TB columns (k_pack_cols)
 
-// Column data of one step: df_b * s, dg_b * s, s_k / s_{k-1}, and the factor
-// invn_b / s (1, or 0 for a flat column) -- see k_pack_cols.
+// Column data of one step (k_pack_cols: {df_b, dg_b, invn_b, nmin8}), the
+// incoming diagonal of lane 0 (edge ring) and of lanes 1..31 (shuffle)
 struct StepIn {
-  double dfb, dgb, rk, kf, e, in;
+  double dfb, dgb, e, in;
 };
 
 __device__ __forceinline__ void prefetch(const double4* cb, const double* ep, double v7, StepIn& d) {
-  const double4 c = *cb;
+  const double2 c = *reinterpret_cast<const double2*>(cb);
   d.dfb = c.x;
   d.dgb = c.y;
-  d.rk = c.z;
-  d.kf = c.w;
   d.e = *ep;
   d.in = shfl_up1(v7);
 }
 
 template <int R>
 struct SweepState {
-  double P[R];   // slot registers: step k, slot r at P[(r - k) mod R]
-  double bK[R];  // best K = cov * invn_b per slot (row factor invn_a left out)
-  int thr[R];    // slot_thr(bK); the best column lives in sm.bj (written on update only)
-  StepIn nx;     // prefetched inputs of the next step
+  double P[R];    // slot registers: step k, slot r at P[(r - k) mod R]
+  double bKp[R];  // kplus(bestK); bestK itself and its column live in sm.bK / sm.bj
+  int thr[R];     // hi(bKp * nmin) of the current block
+  StepIn nx;      // prefetched inputs of the next step
 };
 
 // One block of R steps starting at k0 (k0 % R == 0, R | 32). FIRST: block 0,
@@ -344,32 +352,30 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
   const int ebase = m96;                                    // ring position of E[k0]
   double* const st_prev = sbase + (m96 == 0 ? 95 : m96 - 1);  // E[k0-1]
   double* const st_cur = sbase + ebase;
+  double nmin = 0.0;
 #pragma unroll
   for (int u = 0; u < R; ++u) {
     const int k = k0 + u;
     if (GUARD && k >= n) break;
     const int ph = (R - u) & (R - 1);  // physical register of slot 0 at this step
-    const double kf = S.nx.kf;         // invn_b / s (1, or 0 for a flat column)
+    if (u % TB == 0) {  // threshold block of TB columns
+      nmin = ccur[u].w;
+#pragma unroll
+      for (int r = 0; r < R; ++r) S.thr[r] = __double2hiint(S.bKp[r] * nmin);
+    }
     if (!(FIRST && u == 0)) {
       // fold in the incoming diagonal; lane 31 retires its bottom-row value (column k-1)
       (u == 0 ? st_prev : st_cur + u - 1)[0] = S.P[ph];
       S.P[ph] = l0 ? S.nx.e : S.nx.in;
-      const double dfb = S.nx.dfb, dgb = S.nx.dgb, rk = S.nx.rk;
-      // normalised recurrence c~(i,k) = c~(i-1,k-1) * s_k / s_{k-1} + (df_a dg_b + dg_a df_b) * s_k
-      // (profiles.hpp:330 scaled by s_k = invn_b[k]); only the last FMA depends on the previous step
+      const double dfb = S.nx.dfb, dgb = S.nx.dgb;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         double& c = S.P[(r + ph) & (R - 1)];
-        const double t = __fma_rn(dfa[r], dgb, dga[r] * dfb);
-        c = __fma_rn(c, rk, t);
+        c = __fma_rn(dga[r], dfb, __fma_rn(dfa[r], dgb, c));  // profiles.hpp:330
       }
     }
     if (!GUARD || k + 1 < n)
       prefetch(u + 1 < R ? ccur + u + 1 : cnext, &sm.ering[ebase + u], S.P[(ph + R - 1) & (R - 1)], S.nx);
-    // c~ = cov * invn_b = K for non-flat columns: test its high word directly
-    bool p[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) p[r] = __double2hiint(S.P[(r + ph) & (R - 1)]) >= S.thr[r];
 #ifdef TSD_ABL_NOEXACT
     if (vote_any8(S.P, ph, S.thr) && cx.ncol < 0) [[unlikely]] {
 #else
@@ -380,22 +386,23 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
       if (lane == 0 && cx.first_seg) atomicAdd(&g_exact_first, 1ull);
 #endif
       // exact update: strict K > bestK (columns arrive in increasing order,
-      // so ties keep the lower column, profiles.hpp:70-77); flat column -> K = 0
+      // so ties keep the lower column, profiles.hpp:70-77); a flat column has
+      // invn_b = 0 -> K = 0 (profiles.hpp:332-336)
+      const double invb = ccur[u].z;
       const int col = cx.colbase + k;
-      {
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const double K = S.P[(r + ph) & (R - 1)] * kf;
-          bool ok = K > S.bK[r] && (p[r] || kf == 0.0);
-          if (SELF) {
-            const long long d = cx.row0 + r - col;
-            ok = ok && (d > cx.excl || d < -cx.excl);  // profiles.hpp:281-284
-          }
-          if (ok) {
-            S.bK[r] = K;
-            sm.bj[r][lane] = col;
-            S.thr[r] = slot_thr(K);
-          }
+      for (int r = 0; r < R; ++r) {
+        const double K = S.P[(r + ph) & (R - 1)] * invb;
+        bool ok = K > sm.bK[r][lane];
+        if (SELF) {
+          const long long d = cx.row0 + r - col;
+          ok = ok && (d > cx.excl || d < -cx.excl);  // profiles.hpp:281-284
+        }
+        if (ok) {
+          sm.bK[r][lane] = K;
+          sm.bj[r][lane] = col;
+          S.bKp[r] = kplus(K);
+          S.thr[r] = __double2hiint(S.bKp[r] * nmin);
         }
       }
     }
@@ -420,7 +427,6 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   cp_wait<1>();
   __syncwarp();
   int flushed = 0;  // edge blocks [0, flushed) written back
-  S.nx.kf = sm.colbuf[0][0].w;  // step 0 (heads) only needs the flat factor
   // blocks of R steps; every 32 / R blocks the next block opens chunk c:
   // make it resident, retire edge block c-2, start loading chunk c+1 (3-deep
   // rings keep the in-use slots intact)
@@ -748,11 +754,12 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               const int q = q0 + R * lane + r;
-              // stored in the scale of column q - delta: the consumer multiplies
-              // by s_{k}/s_{k-1} (delta = 1: row 0 adds nothing, so c~(0,q) =
-              // E[q-1] * s_q / s_{q-1} must hold)
+              // delta = 1: row 0 adds nothing, so cov(0, q) = E[q-1]; FP32
+              // stores it in the scale of column q - delta (its consumer
+              // multiplies by s_k / s_{k-1})
               if (q < sg.ncol - 1 + delta) {
-                const double v = (out[r] - (a.mub[sg.col0 + q] - cS) * eU) * a.scale[sg.col0 + q - delta];
+                const double v =
+                    (out[r] - (a.mub[sg.col0 + q] - cS) * eU) * (F32 ? a.scale[sg.col0 + q - delta] : 1.0);
                 if constexpr (F32)
                   reinterpret_cast<float*>(cx.E)[q - delta] = (float)v;
                 else
@@ -772,6 +779,11 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
             head[2 * r] = h2.x;
             head[2 * r + 1] = h2.y;
           }
+          if constexpr (F32) {  // the FP32 sweep runs the column-normalised recurrence
+            const double s0 = a.scale[sg.col0];
+#pragma unroll
+            for (int r = 0; r < R; ++r) head[r] *= s0;
+          }
         } else {  // left edge: cov(i, col0) for the band's rows, batched 8 segments at a time
 #ifndef TSD_ABL_NOHEADS
           if (((s - s_beg) & 7) == 0 && a.dmma_heads)
@@ -787,7 +799,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           } else {
             sliding_dot<R>(sm, a.btil + (int64_t)s * a.m, 0.0, a.xa + i0, a.na - i0, cA, a.m, lane, out, nullptr);
           }
-          const double e = a.ebt[s], s0 = a.scale[sg.col0];
+          const double e = a.ebt[s], s0 = F32 ? a.scale[sg.col0] : 1.0;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const int64_t i = i0 + R * lane + r;
@@ -839,12 +851,9 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
             const bool in = i < a.nrows;
             dfa[r] = in ? a.dfa[i] : 0.0;
             dga[r] = in ? a.dga[i] : 0.0;
-            S.bK[r] = sm.bK[r][lane];
-            S.thr[r] = slot_thr(S.bK[r]);
+            S.bKp[r] = kplus(sm.bK[r][lane]);
           }
           sweep_segment<R, SELF>(sm, cx, lane, dfa, dga, S);
-#pragma unroll
-          for (int r = 0; r < R; ++r) sm.bK[r][lane] = S.bK[r];
         }
       }
       // band results: c = clamp(K * invn_a) (profiles.hpp:331, :335)
@@ -883,27 +892,29 @@ __global__ void k_merge_groups(double* __restrict__ c, int64_t* __restrict__ j, 
   j[i] = bj;
 }
 
-// Column data for the normalised recurrence (one double4 per concatenated
-// column j): the sweep tracks c~(i,j) = cov(i,j) * s_j with s_j = invn_b[j]
-// (s_j = 1 for flat or straddling windows, so the scale never vanishes):
-//   {df_b[j] * s_j, dg_b[j] * s_j, s_j / s_{j-1}, invn_b[j] / s_j}
-// and scale[j] = s_j for the heads / top edges.
+// FP64 column data per concatenated window j: {df_b, dg_b, invn_b, nmin8}
+// with nmin8 = (1 - 2^-40) x the smallest window norm 1/invn_b over windows
+// j .. j+7 (flat or straddling windows count as DBL_MAX): the block
+// threshold of the sweep, whose blocks start at multiples of 8 of a
+// segment's columns. scale[j] (s_j = invn_b, 1 if flat) serves the FP32 path.
 __global__ void k_pack_cols(const double* __restrict__ df, const double* __restrict__ dg,
-                            const double* __restrict__ invn, int64_t n, double4* __restrict__ col,
-                            double* __restrict__ scale) {
+                            const double* __restrict__ invn, const uint8_t* __restrict__ flag, int64_t n,
+                            double4* __restrict__ col, double* __restrict__ scale) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n + 64) return;
   if (i >= n) {
-    col[i] = make_double4(0, 0, 1, 0);
+    col[i] = make_double4(0, 0, 0, DBL_MAX);
     scale[i] = 1.0;
     return;
   }
+  double nm = DBL_MAX;
+  for (int t = 0; t < TB && i + t < n; ++t) {
+    const double iv = invn[i + t];
+    if ((flag[i + t] & 1) && iv > 0.0) nm = fmin(nm, 1.0 / iv);
+  }
   const double iv = invn[i];
-  const double sj = iv > 0.0 ? iv : 1.0;
-  const double ivp = i > 0 ? invn[i - 1] : 0.0;
-  const double sp = ivp > 0.0 ? ivp : 1.0;
-  col[i] = make_double4(df[i] * sj, dg[i] * sj, sj / sp, iv > 0.0 ? 1.0 : 0.0);
-  scale[i] = sj;
+  col[i] = make_double4(df[i], dg[i], iv, nm < DBL_MAX ? nm * (1.0 - 0x1p-40) : DBL_MAX);
+  scale[i] = iv > 0.0 ? iv : 1.0;
 }
 
 // FP32 column data (Col32 layout in the same 32-byte slots), from FP64 values
@@ -1174,8 +1185,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     k_pack_cols32<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(in.cols.df, in.cols.dg, in.cols.invn,
                                                                               in.cols.nwin, d_col, d_scale);
   else
-    k_pack_cols<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(in.cols.df, in.cols.dg, in.cols.invn,
-                                                                            in.cols.nwin, d_col, d_scale);
+    k_pack_cols<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(
+        in.cols.df, in.cols.dg, in.cols.invn, in.cols.flag, in.cols.nwin, d_col, d_scale);
   ++nl;
   k_btil<<<nseg, 128, 0, st>>>(in.xb, in.cols.mu, d_segs, m, d_btil, d_ebt);
   ++nl;
@@ -1194,8 +1205,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       d_seed = F32 ? nullptr : (unsigned long long*)arena.get(sizeof(unsigned long long) * nrows);
       if (d_heads && (F32 || d_seed)) {
         const int rc = compute_heads_fft(in.xa, in.na, nrows, hstride, in.rows.mu, in.rows.flag, d_btil, d_ebt,
-                                         d_scale, d_col, d_segs, nseg, m, d_heads, hstride, d_seed, arena, st, &nl,
-                                         err);
+                                         d_col, d_segs, nseg, m, d_heads, hstride, d_seed, arena, st, &nl, err);
         if (rc != kOk) return rc;
       }
     }

@@ -118,8 +118,7 @@ int heads_fft_supported(int m);
 // column-0 candidate max_s head * kf over ALL segments (0 = none); one ulp
 // below it is a strict lower bound the join starts from (join.cu, k_join).
 int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrows, const double* d_mua,
-                      const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double* d_scale,
-                      const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
+                      const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
                       unsigned long long* d_seed, Arena& arena, cudaStream_t st, int* launches, Error* err);
 
 // Epilogue: corr -> distance (series.hpp:153-161), concat column -> source
