@@ -113,19 +113,46 @@ __device__ __forceinline__ void dft16(double2 (&v)[16]) {
 // One Stockham pass (radix 16) reading thread j's inputs j + 256 r from
 // registers v. Ns = size of the sub-transforms already done (1, 16, 256).
 // Pass Ns < 256 writes its outputs to shared memory; the caller syncs.
+// twiddle exp(-2 pi i t / N) from the shared half table (t + N/2 -> negated)
+__device__ __forceinline__ double2 twiddle(const double2* __restrict__ stw, int t) {
+  const double2 w = stw[t & (FFT_N / 2 - 1)];
+  return (t & (FFT_N / 2)) ? make_double2(-w.x, -w.y) : w;
+}
+
 template <bool INV>
-__device__ __forceinline__ void pass_compute(double2 (&v)[16], int j, int Ns, const double2* __restrict__ tw) {
+__device__ __forceinline__ void pass_compute(double2 (&v)[16], int j, int Ns, const double2* __restrict__ stw) {
   if (Ns > 1) {
-    const int k = j & (Ns - 1);
-    const int step = FFT_N / (Ns * 16);
+    // w^r for r = 1..15 from four table entries (w, w^2, w^4, w^8; r k step < N)
+    // and products of at most three of them
+    const int t1 = (j & (Ns - 1)) * (FFT_N / (Ns * 16));
+    double2 w[16];
+    w[1] = twiddle(stw, t1);
+    w[2] = twiddle(stw, 2 * t1);
+    w[4] = twiddle(stw, 4 * t1);
+    w[8] = twiddle(stw, 8 * t1);
+    w[3] = cmul(w[1], w[2]);
+    w[5] = cmul(w[1], w[4]);
+    w[6] = cmul(w[2], w[4]);
+    w[7] = cmul(w[3], w[4]);
+    w[9] = cmul(w[1], w[8]);
+    w[10] = cmul(w[2], w[8]);
+    w[11] = cmul(w[3], w[8]);
+    w[12] = cmul(w[4], w[8]);
+    w[13] = cmul(w[5], w[8]);
+    w[14] = cmul(w[6], w[8]);
+    w[15] = cmul(w[7], w[8]);
 #pragma unroll
     for (int r = 1; r < 16; ++r) {
-      double2 w = __ldg(&tw[(r * k * step) & (FFT_N - 1)]);
-      if (INV) w.y = -w.y;
-      v[r] = cmul(v[r], w);
+      if (INV) w[r].y = -w[r].y;
+      v[r] = cmul(v[r], w[r]);
     }
   }
   dft16<INV>(v);
+}
+
+// stage the half twiddle table (global, k_fft_twiddles) in shared memory
+__device__ __forceinline__ void load_twiddles(double2* __restrict__ stw, const double2* __restrict__ tw) {
+  for (int t = threadIdx.x; t < FFT_N / 2; t += blockDim.x) stw[t] = tw[t];
 }
 
 __device__ __forceinline__ void pass_store(double2* __restrict__ sm, const double2 (&v)[16], int j, int Ns) {
@@ -141,18 +168,18 @@ __device__ __forceinline__ void pass_load(const double2* __restrict__ sm, double
 
 // Full transform of v (thread j holds inputs j + 256 r) -> v (outputs j + 256 r)
 template <bool INV>
-__device__ __forceinline__ void fft4096(double2 (&v)[16], double2* sm, int j, const double2* __restrict__ tw) {
-  pass_compute<INV>(v, j, 1, tw);
+__device__ __forceinline__ void fft4096(double2 (&v)[16], double2* sm, int j, const double2* __restrict__ stw) {
+  pass_compute<INV>(v, j, 1, stw);
   __syncthreads();  // previous readers of sm are done
   pass_store(sm, v, j, 1);
   __syncthreads();
   pass_load(sm, v, j);
-  pass_compute<INV>(v, j, 16, tw);
+  pass_compute<INV>(v, j, 16, stw);
   __syncthreads();
   pass_store(sm, v, j, 16);
   __syncthreads();
   pass_load(sm, v, j);
-  pass_compute<INV>(v, j, 256, tw);
+  pass_compute<INV>(v, j, 256, stw);
 }
 
 __global__ void k_fft_twiddles(double2* tw) {
@@ -169,6 +196,8 @@ __global__ void __launch_bounds__(FFT_T, 1)
     k_pair_spectra(const double* __restrict__ btil, int nseg, int m, const double2* __restrict__ tw,
                    double2* __restrict__ spec) {
   extern __shared__ double2 fsm[];
+  double2* stw = fsm + FFT_PAD;
+  load_twiddles(stw, tw);
   const int p = blockIdx.x, j = threadIdx.x;
   const int s0 = 2 * p, s1 = 2 * p + 1;
   double2 v[16];
@@ -179,7 +208,7 @@ __global__ void __launch_bounds__(FFT_T, 1)
     const double b = (k < m && s1 < nseg) ? btil[(int64_t)s1 * m + k] : 0.0;
     v[r] = make_double2(a, b);
   }
-  fft4096<false>(v, fsm, j, tw);
+  fft4096<false>(v, fsm, j, stw);
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     const int f = (FFT_N - (j + 256 * r)) & (FFT_N - 1);
@@ -212,51 +241,73 @@ __device__ __forceinline__ unsigned long long order_key(double v) {
   return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
+__device__ __forceinline__ void cp16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(sdst)),
+               "l"(gsrc));
+}
+
+// Shared memory: FFT work buffer (padded) | next pair spectrum (cp.async) |
+// half twiddle table | per-row mean offsets. Thread j only ever touches
+// spectrum / offset entries j + 256 r, so those need no barriers.
+constexpr size_t HEADS_SMEM = sizeof(double2) * (FFT_PAD + FFT_N + FFT_N / 2) + sizeof(double) * FFT_N;
+
 __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
   extern __shared__ double2 fsm[];
-  double* mk = reinterpret_cast<double*>(fsm + FFT_PAD);  // per-row running max of head * kf
+  double2* zbuf = fsm + FFT_PAD;
+  double2* stw = zbuf + FFT_N;
+  double* dmu = reinterpret_cast<double*>(stw + FFT_N / 2);
   const int j = threadIdx.x;
   const int64_t blk0 = (int64_t)blockIdx.x * a.Q;
   const int p0 = blockIdx.y * a.ppc, p1 = min(a.npairs, p0 + a.ppc);
+  auto fetch = [&](int p) {
+    const double2* sp = a.spec + (int64_t)p * FFT_N;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) cp16(&zbuf[j + 256 * r], &sp[j + 256 * r]);
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  fetch(p0);
+  load_twiddles(stw, a.tw);
   const double c = a.mua[blk0];  // centring constant of the block (any value is exact)
   double2 X[16];
+  double mk[16];  // per-row running max of head * invn_b(col0)
 #pragma unroll
   for (int r = 0; r < 16; ++r) {
     const int64_t n = blk0 + j + 256 * r;
     X[r] = make_double2((n < a.na ? a.x[n] : c) - c, 0.0);
-    mk[j + 256 * r] = -INFINITY;
+    dmu[j + 256 * r] = (n < a.nrows ? a.mua[n] : c) - c;
+    mk[r] = -INFINITY;
   }
-  fft4096<false>(X, fsm, j, a.tw);
+  __syncthreads();  // twiddles staged
+  fft4096<false>(X, fsm, j, stw);
   const double invN = 1.0 / FFT_N;
   for (int p = p0; p < p1; ++p) {
-    double2 v[16];
-    const double2* sp = a.spec + (int64_t)p * FFT_N;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = cmul(X[r], __ldg(&sp[j + 256 * r]));
-    fft4096<true>(v, fsm, j, a.tw);
     const int s0 = 2 * p, s1 = 2 * p + 1;
-    const int64_t c0 = a.segs[s0].col0;
-    const double e0 = a.ebt[s0], k0 = a.seed ? a.col[c0].z : 0.0;
     const bool two = s1 < a.nseg;
-    const int64_t c1 = two ? a.segs[s1].col0 : c0;
-    const double e1 = two ? a.ebt[s1] : 0.0, k1 = (two && a.seed) ? a.col[c1].z : 0.0;
+    const int64_t c0 = a.segs[s0].col0, c1 = two ? a.segs[s1].col0 : c0;
+    const double e0 = a.ebt[s0], e1 = two ? a.ebt[s1] : 0.0;
+    const double k0 = a.seed ? a.col[c0].z : 0.0, k1 = (two && a.seed) ? a.col[c1].z : 0.0;
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    double2 v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = cmul(X[r], zbuf[j + 256 * r]);
+    if (p + 1 < p1) fetch(p + 1);  // own entries only: no barrier needed
+    fft4096<true>(v, fsm, j, stw);
     double* h0 = a.heads + (int64_t)s0 * a.hstride;
     double* h1 = a.heads + (int64_t)s1 * a.hstride;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const int q = j + 256 * r;
       const int64_t i = blk0 + q;
-      const double dmu = (i < a.nrows ? __ldg(&a.mua[i]) : c) - c;
       if (q < a.Q && i < a.hrows) {
-        const double g0 = v[r].x * invN - dmu * e0;
+        const double d = dmu[q];
+        const double g0 = v[r].x * invN - d * e0;
         h0[i] = g0;
-        double best = fmax(mk[q], g0 * k0);
+        mk[r] = fmax(mk[r], g0 * k0);
         if (two) {
-          const double g1 = v[r].y * invN - dmu * e1;
+          const double g1 = v[r].y * invN - d * e1;
           h1[i] = g1;
-          best = fmax(best, g1 * k1);
+          mk[r] = fmax(mk[r], g1 * k1);
         }
-        mk[q] = best;
       }
     }
   }
@@ -265,7 +316,7 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
     for (int r = 0; r < 16; ++r) {
       const int q = j + 256 * r;
       const int64_t i = blk0 + q;
-      if (q < a.Q && i < a.nrows && mk[q] > -INFINITY) atomicMax(&a.seed[i], order_key(mk[q]));
+      if (q < a.Q && i < a.nrows && mk[r] > -INFINITY) atomicMax(&a.seed[i], order_key(mk[r]));
     }
   }
 }
@@ -284,8 +335,8 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
     if (err) *err = Error{kCudaError, "device allocation failed for the FFT heads"};
     return kCudaError;
   }
-  const size_t smem = sizeof(double2) * FFT_PAD;
-  const size_t smem_h = smem + sizeof(double) * FFT_N;
+  const size_t smem = sizeof(double2) * (FFT_PAD + FFT_N / 2);
+  const size_t smem_h = HEADS_SMEM;
   CUDA_TRY(cudaFuncSetAttribute(k_pair_spectra, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   CUDA_TRY(cudaFuncSetAttribute(k_heads_fft, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_h));
   k_fft_twiddles<<<FFT_N / 256, 256, 0, st>>>(d_tw);
