@@ -316,13 +316,20 @@ constexpr int TB = TSD_TB;  // threshold block (columns); nmin spans TB columns 
 // Column data of one step (k_pack_cols: {df_b, dg_b, invn_b, nmin8}), the
 // incoming diagonal of lane 0 (edge ring) and of lanes 1..31 (shuffle)
 struct StepIn {
-  double dfb, dgb, e, in;
+  double dfb, dgb, e, in, nmin;  // nmin: loaded with the first column of a threshold block
 };
 
-__device__ __forceinline__ void prefetch(const double4* cb, const double* ep, double v7, StepIn& d) {
-  const double2 c = *reinterpret_cast<const double2*>(cb);
-  d.dfb = c.x;
-  d.dgb = c.y;
+__device__ __forceinline__ void prefetch(bool nm, const double4* cb, const double* ep, double v7, StepIn& d) {
+  if (nm) {  // constant after unrolling
+    const double4 c = *cb;
+    d.dfb = c.x;
+    d.dgb = c.y;
+    d.nmin = c.w;
+  } else {
+    const double2 c = *reinterpret_cast<const double2*>(cb);
+    d.dfb = c.x;
+    d.dgb = c.y;
+  }
   d.e = *ep;
   d.in = shfl_up1(v7);
 }
@@ -358,8 +365,8 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
     const int k = k0 + u;
     if (GUARD && k >= n) break;
     const int ph = (R - u) & (R - 1);  // physical register of slot 0 at this step
-    if (u % TB == 0) {  // threshold block of TB columns
-      nmin = ccur[u].w;
+    if (u % TB == 0) {  // threshold block of TB columns (nmin prefetched with its first column)
+      nmin = (FIRST && u == 0) ? ccur[0].w : S.nx.nmin;
 #pragma unroll
       for (int r = 0; r < R; ++r) S.thr[r] = __double2hiint(S.bKp[r] * nmin);
     }
@@ -375,7 +382,8 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
       }
     }
     if (!GUARD || k + 1 < n)
-      prefetch(u + 1 < R ? ccur + u + 1 : cnext, &sm.ering[ebase + u], S.P[(ph + R - 1) & (R - 1)], S.nx);
+      prefetch((u + 1) % TB == 0, u + 1 < R ? ccur + u + 1 : cnext, &sm.ering[ebase + u],
+               S.P[(ph + R - 1) & (R - 1)], S.nx);
 #ifdef TSD_ABL_NOEXACT
     if (vote_any8(S.P, ph, S.thr) && cx.ncol < 0) [[unlikely]] {
 #else
