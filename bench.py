@@ -211,7 +211,7 @@ def run_gpu(args):
     if dist:
         dist.barrier()
     launches = 0
-    join_ms = []
+    join_ms, kernel_ms, heads_ms = [], [], []
     elapsed_ms = 0.0
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)
@@ -224,7 +224,10 @@ def run_gpu(args):
             e1.synchronize()
             elapsed_ms += e0.elapsed_time(e1)
             s_ms, j_ms, nl = plan.last_timing()
+            k_ms, h_ms = plan.last_kernel_timing()
             join_ms.append(j_ms)
+            kernel_ms.append(k_ms)
+            heads_ms.append(h_ms)
             launches += nl
         torch.cuda.synchronize(dev)
     if dist:
@@ -276,12 +279,20 @@ def run_gpu(args):
         return 0
     peak = tsd.measure_peak("fp64", seconds=2.0)
     jms = statistics.median(join_ms)
-    achieved = FLOPS_PER_CELL * cells_per_step() / (jms * 1e-3)
+    kms = statistics.median(kernel_ms)
+    hms = statistics.median(heads_ms)
+    achieved = FLOPS_PER_CELL * cells_per_step() / (kms * 1e-3)
+    traffic = args.traffic if args.traffic is not None else committed_traffic()
     roofline = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
-                "frac": achieved / peak, "traffic": args.traffic,
-                "kernel": "k_join_f64 (+ its edge/merge helpers)", "achieved_def":
-                    "6 FP64 flops per valid cell (profiles.hpp:330-331) x cells per launch / median join time "
-                    "(CUDA events on the launching stream)",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": "k_join<8,false,false> (FP64 row-band join)", "achieved_def":
+                    "6 FP64 flops per valid cell (profiles.hpp:330-331) x cells per launch / median duration of "
+                    "the join kernel (CUDA events around its launch, on the launching stream)",
+                "traffic_def": "dram__bytes_read.sum + dram__bytes_write.sum of one k_join launch, ncu --set full "
+                               "capture of this bench command (profiles/r1_k_join_traffic.json)",
+                "pipeline": {"join_ms_median": jms, "kernel_ms_median": kms, "heads_fft_ms_median": hms,
+                             "frac": FLOPS_PER_CELL * cells_per_step() / (jms * 1e-3) / peak,
+                             "def": "the whole join phase (column packing, FFT heads, join kernel, group merge)"},
                 "peak_def": "DFMA throughput measured live by tsd_measure_peak (2 s sustained, this GPU); "
                             "MEASURED_PEAKS.json has no FP64 entry"}
     cpu = cpu_reference_gcells(q, segs, os.cpu_count() or 1) if world == 1 or rank == 0 else None
@@ -301,6 +312,17 @@ def run_gpu(args):
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def committed_traffic():
+    """DRAM bytes per k_join launch from the committed ncu capture of this workload, or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_k_join_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["dram_bytes_per_launch"]) if d.get("workload") == workload_config()["workload"] else None
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def main():

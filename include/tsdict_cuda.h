@@ -105,6 +105,11 @@ int tsd_dict_plan_destroy(tsd_dict_plan* plan);
  * alone, plus the number of kernel launches that call issued. */
 int tsd_dict_plan_last_timing(tsd_dict_plan* plan, double* step_ms, double* join_ms, int* launches);
 
+/* CUDA-event device times (ms) of the last join call of this plan for the
+ * row-band join kernel alone and for the FFT heads pre-pass (0 when the
+ * heads were computed inside the join kernel). */
+int tsd_dict_plan_last_kernel_timing(tsd_dict_plan* plan, double* join_kernel_ms, double* heads_ms);
+
 /* ---- diagnostics ---- */
 const char* tsd_last_error(void);
 const char* tsd_status_name(int status); /* reference errc_name (errors.hpp:37-57) */

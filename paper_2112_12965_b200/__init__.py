@@ -100,6 +100,7 @@ C_SYMBOLS = {
     "tsd_dict_plan_join": (_int, [_vp, _f64p, _szp, _sz, _f64p, _i64p]),
     "tsd_dict_plan_destroy": (_int, [_vp]),
     "tsd_dict_plan_last_timing": (_int, [_vp, _f64p, _f64p, ctypes.POINTER(_int)]),
+    "tsd_dict_plan_last_kernel_timing": (_int, [_vp, _f64p, _f64p]),
     "tsd_last_error": (ctypes.c_char_p, []),
     "tsd_status_name": (ctypes.c_char_p, [_int]),
     "tsd_build_info": (ctypes.c_char_p, []),
@@ -337,6 +338,12 @@ class DictPlan:
         s, j, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
         _check(self._lib.tsd_dict_plan_last_timing(self._h, ctypes.byref(s), ctypes.byref(j), ctypes.byref(n)))
         return s.value, j.value, n.value
+
+    def last_kernel_timing(self):
+        """(join kernel ms, FFT heads pre-pass ms) of the last join call (CUDA events)."""
+        k, h = ctypes.c_double(), ctypes.c_double()
+        _check(self._lib.tsd_dict_plan_last_kernel_timing(self._h, ctypes.byref(k), ctypes.byref(h)))
+        return k.value, h.value
 
     def close(self):
         if self._h:

@@ -65,7 +65,7 @@ int fail(const Error& e) { return fail(e.code, e.msg); }
 
 struct Stream {
   cudaStream_t st = nullptr;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[8] = {};  // 0..3: step / join phases; 4..7: heads pre-pass and join kernel
   int init() {
     if (st) return kOk;
     int n = 0;
@@ -121,7 +121,7 @@ struct tsd_dict_plan {
   int64_t nb = 0;
   WindowArrays cols;
   bool dict_nonfinite = false;
-  double step_ms = 0.0, join_ms = 0.0;
+  double step_ms = 0.0, join_ms = 0.0, kernel_ms = 0.0, heads_ms = 0.0;
   int launches = 0;
 };
 
@@ -208,6 +208,7 @@ int plan_join_dev(tsd_dict_plan* p, const double* d_q, const size_t* q_len, size
   CK(cudaMemcpyAsync(d_woff, woff.data(), sizeof(int64_t) * nser, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_ooff, ooff.data(), sizeof(int64_t) * nser, cudaMemcpyHostToDevice, st));
   int launches = 5;  // stats kernels
+  for (int e = 4; e < 8; ++e) in.ev[e - 4] = p->s.ev[e];
   CK(cudaEventRecord(p->s.ev[1], st));
   TRY(run_join(in, d_bc, d_bj, ar, st, &er, &launches));
   CK(cudaEventRecord(p->s.ev[2], st));
@@ -221,6 +222,10 @@ int plan_join_dev(tsd_dict_plan* p, const double* d_q, const size_t* q_len, size
   cudaEventElapsedTime(&b, p->s.ev[1], p->s.ev[2]);
   p->step_ms = a;
   p->join_ms = b;
+  float kk = 0, hh = 0;
+  cudaEventElapsedTime(&kk, p->s.ev[6], p->s.ev[7]);
+  p->kernel_ms = kk;
+  p->heads_ms = in.heads_used && cudaEventElapsedTime(&hh, p->s.ev[4], p->s.ev[5]) == cudaSuccess ? hh : 0.0;
   p->launches = launches;
   CK(cudaGetLastError());
   return kOk;
@@ -427,6 +432,13 @@ int tsd_dict_plan_join(tsd_dict_plan* plan, const double* q, const size_t* q_len
 
 int tsd_dict_plan_destroy(tsd_dict_plan* plan) {
   delete plan;
+  return kOk;
+}
+
+int tsd_dict_plan_last_kernel_timing(tsd_dict_plan* plan, double* join_kernel_ms, double* heads_ms) {
+  if (!plan) return fail(kInvalidArgument, "null plan");
+  if (join_kernel_ms) *join_kernel_ms = plan->kernel_ms;
+  if (heads_ms) *heads_ms = plan->heads_ms;
   return kOk;
 }
 

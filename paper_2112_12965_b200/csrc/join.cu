@@ -300,9 +300,10 @@ __device__ __forceinline__ void flush_block(WarpSmem<R>& sm, const SweepCtx& cx,
 // and a row test without a per-cell multiply: the candidate K = cov * invn_b
 // (row factor invn_a left out) can beat bestK > 0 only if
 //   cov > bestK / invn_b >= bestK * nmin(block),
-// nmin = (1 - 2^-40) x the smallest window norm among the block's 8 columns
-// (k_pack_cols; the factor absorbs the roundings of the exact test). The
-// threshold is compared on high words (integer pipe): thr = hi(bestK+ * nmin)
+// nmin = (1 - 2^-40) x the smallest window norm among the TB = 4 columns of
+// the threshold block (k_pack_cols; the factor absorbs the roundings of the
+// exact test). The threshold is compared on high words (integer pipe):
+// thr = hi(bestK+ * nmin)
 // with bestK+ = bestK if bestK > 0, else -0.0, whose product -0.0 has high
 // word INT_MIN (passes everything). Inactive rows carry bestK = +inf
 // (thr = hi(inf), never passed by a finite cov). A pass runs the exact update
@@ -313,7 +314,7 @@ __device__ __forceinline__ double kplus(double bK) { return bK > 0.0 ? bK : -0.0
 #endif
 constexpr int TB = TSD_TB;  // threshold block (columns); nmin spans TB columns (k_pack_cols)
 
-// Column data of one step (k_pack_cols: {df_b, dg_b, invn_b, nmin8}), the
+// Column data of one step (k_pack_cols: {df_b, dg_b, invn_b, nmin}), the
 // incoming diagonal of lane 0 (edge ring) and of lanes 1..31 (shuffle)
 struct StepIn {
   double dfb, dgb, e, in, nmin;  // nmin: loaded with the first column of a threshold block
@@ -900,10 +901,10 @@ __global__ void k_merge_groups(double* __restrict__ c, int64_t* __restrict__ j, 
   j[i] = bj;
 }
 
-// FP64 column data per concatenated window j: {df_b, dg_b, invn_b, nmin8}
-// with nmin8 = (1 - 2^-40) x the smallest window norm 1/invn_b over windows
-// j .. j+7 (flat or straddling windows count as DBL_MAX): the block
-// threshold of the sweep, whose blocks start at multiples of 8 of a
+// FP64 column data per concatenated window j: {df_b, dg_b, invn_b, nmin}
+// with nmin = (1 - 2^-40) x the smallest window norm 1/invn_b over windows
+// j .. j+TB-1 (flat or straddling windows count as DBL_MAX): the block
+// threshold of the sweep, whose blocks start at multiples of TB of a
 // segment's columns. scale[j] (s_j = invn_b, 1 if flat) serves the FP32 path.
 __global__ void k_pack_cols(const double* __restrict__ df, const double* __restrict__ dg,
                             const double* __restrict__ invn, const uint8_t* __restrict__ flag, int64_t n,
@@ -1212,9 +1213,12 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       d_heads = (double*)arena.get(hbytes);
       d_seed = F32 ? nullptr : (unsigned long long*)arena.get(sizeof(unsigned long long) * nrows);
       if (d_heads && (F32 || d_seed)) {
+        if (in.ev[0]) CUDA_TRY(cudaEventRecord(in.ev[0], st));
+        in.heads_used = true;
         const int rc = compute_heads_fft(in.xa, in.na, nrows, hstride, in.rows.mu, in.rows.flag, d_btil, d_ebt,
                                          d_col, d_segs, nseg, m, d_heads, hstride, d_seed, arena, st, &nl, err);
         if (rc != kOk) return rc;
+        if (in.ev[1]) CUDA_TRY(cudaEventRecord(in.ev[1], st));
       }
     }
   }
@@ -1261,8 +1265,10 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   cudaMemcpyToSymbol(g_exact_first, &zero, 8);
   cudaMemcpyToSymbol(g_step_first, &zero, 8);
 #endif
+  if (in.ev[2]) CUDA_TRY(cudaEventRecord(in.ev[2], st));
   kern<<<grid, 32 * WARPS, smem_bytes, st>>>(a);
   ++nl;
+  if (in.ev[3]) CUDA_TRY(cudaEventRecord(in.ev[3], st));
 #ifdef TSD_COUNT_EXACT
   {
     unsigned long long ce = 0, cs = 0;

@@ -102,6 +102,10 @@ struct JoinInputs {
   int m;
   int64_t excl = -1;  // self-join exclusion half-width (|i-j| <= excl rejected); -1 = AB join
   int precision;      // 0 fp64, 1 fp32
+  // optional timing events: [0, 1] around the FFT heads pre-pass, [2, 3]
+  // around the join kernel (recorded when non-null); heads_used set by run_join
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  mutable bool heads_used = false;
 };
 
 // Runs the row-band join of every row against every valid column of every
