@@ -1296,12 +1296,48 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
 
 }  // namespace
 
+namespace {
+// FP32 mode: the FP32 sweep chooses each row's column; its correlation is
+// then recomputed exactly in FP64 as a direct m-term dot product of the two
+// centred windows (window_dot, profiles.hpp:101-108). Without this the
+// distance sqrt(2m(1 - rho)) of a near-exact match amplifies FP32 rounding
+// of rho (~1e-7) to ~3e-3. Flat rows are resolved by the epilogue; a flat
+// column keeps rho = 0 (profiles.hpp:332-336).
+__global__ void k_refine_fp64(double* __restrict__ bc, const int64_t* __restrict__ bj, int64_t nrows,
+                              const double* __restrict__ xa, const double* __restrict__ mua,
+                              const double* __restrict__ invn_a, const uint8_t* __restrict__ flag_a,
+                              const double* __restrict__ xb, const double* __restrict__ mub,
+                              const double* __restrict__ invn_b, int m) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  const int64_t j = bj[i];
+  if (j < 0 || flag_a[i] != 1 || !(invn_b[j] > 0.0)) return;
+  const double ma = mua[i], mb = mub[j];
+  double acc = 0.0;
+  for (int k = 0; k < m; ++k) acc = __fma_rn(xa[i + k] - ma, xb[j + k] - mb, acc);
+  bc[i] = clamp_corr(acc * invn_a[i] * invn_b[j]);
+}
+}  // namespace
+
 int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st, Error* err,
              int* launches) {
   const bool self = in.excl >= 0;
-  if (in.precision == 1)
-    return self ? launch_join<8, true, true>(in, d_best_c, d_best_j, arena, st, err, launches)
-                : launch_join<8, false, true>(in, d_best_c, d_best_j, arena, st, err, launches);
+  if (in.precision == 1) {
+    const int rc = self ? launch_join<8, true, true>(in, d_best_c, d_best_j, arena, st, err, launches)
+                        : launch_join<8, false, true>(in, d_best_c, d_best_j, arena, st, err, launches);
+    if (rc != kOk) return rc;
+    const int64_t n = in.rows.nwin;
+    k_refine_fp64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_best_c, d_best_j, n, in.xa, in.rows.mu,
+                                                               in.rows.invn, in.rows.flag, in.xb, in.cols.mu,
+                                                               in.cols.invn, in.m);
+    if (launches) ++*launches;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      if (err) *err = Error{kCudaError, cudaGetErrorString(e)};
+      return kCudaError;
+    }
+    return kOk;
+  }
   return self ? launch_join<8, true, false>(in, d_best_c, d_best_j, arena, st, err, launches)
               : launch_join<8, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
 }

@@ -194,6 +194,42 @@ def test_fft_heads_vs_direct_heads_and_oracle(monkeypatch, m, nseg, L):
     check_profile(P.values, P.indices, rv, ri, m, dd, label=f"fft vs oracle m={m}")
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_adversarial_dictionary_thresholds_and_seeds(precision):
+    """Edge cases of the row test and the head seeds, against the oracle:
+    rows whose every candidate is anti-correlated (bestK <= 0 -> threshold
+    pass-all), flat windows at a segment's column 0 (K = 0 candidates, the
+    only non-negative ones for those rows), single-window segments (ncol = 1,
+    head only), a segment repeating the query exactly (ties at distance 0 at
+    several columns: lowest index wins), and windows whose norms change by
+    orders of magnitude inside one 4-column threshold block."""
+    m = 32
+    t = np.arange(6000)
+    q = np.sin(2 * np.pi * t / 97.0) + 0.01 * synth.Rng(41).noise(6000)
+    anti = -np.sin(2 * np.pi * np.arange(700) / 97.0)          # anti-correlated with most rows
+    flat_head = np.concatenate([np.full(40, 3.0), anti[:300]])  # flat windows at column 0..8
+    single = anti[5:5 + m]                                      # exactly one window
+    rep = np.tile(q[100:100 + 97], 5)                           # exact repeats -> ties
+    steps = np.concatenate([np.full(50, 1.0), 1e-6 * synth.Rng(42).noise(60), 1e3 * synth.Rng(43).noise(60),
+                            np.full(20, -2.0)])                 # wildly varying window norms
+    segs = [anti, flat_head, single, rep, steps]
+    starts = [0, 1000, 2000, 3000, 4000]
+    D = _dict(segs, starts, m)
+    # query rows that see only anti-correlated / flat candidates: the query
+    # against the first three segments alone
+    for sub in ([0, 1, 2], [0, 2], [1], [3], [4], [0, 1, 2, 3, 4]):
+        ss = [segs[k] for k in sub]
+        st = [starts[k] for k in sub]
+        Dk = _dict(ss, st, m)
+        P = tsd.join_dictionary(q, Dk, m, precision=precision)
+        rv, ri = O.dict_join(q, ss, st, m)
+        if precision == "fp64":
+            check_profile(P.values, P.indices, rv, ri, m, dict_dist(q, ss, st, m), label=f"adversarial {sub}")
+        else:
+            assert np.max(np.abs(P.values - rv)) < 1e-3, f"fp32 adversarial {sub}"
+    assert D.m == m
+
+
 def test_batched_C5_shape():
     """BASELINE C5 shape: transport-like series vs one shared 64 x 1024 dictionary,
     m = 128, one device pass; each series equals its own join_dictionary oracle"""
