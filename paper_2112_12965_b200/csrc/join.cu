@@ -1088,7 +1088,29 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
                 int* launches) {
   constexpr int H = Geo<R>::H;
   const int m = in.m;
-  const int nseg = (int)in.segs.size();
+  // Virtual segments: a long segment (self-join, AB-join against one long
+  // series) is cut into contiguous column pieces so the decomposition can form
+  // several segment groups and tall tasks (few top edges). Column numbering,
+  // masks and the epilogue's source mapping are unchanged; each piece starts
+  // from its own head (cov at its first column), exactly as a segment does.
+  std::vector<SegDev> vsegs;
+  {
+    int64_t tot = 0;
+    for (const auto& s : in.segs) tot += s.ncol;
+    const int64_t lmax = std::max<int64_t>(8192, (tot + 63) / 64);
+    for (const auto& s : in.segs) {
+      const int64_t np = (s.ncol + lmax - 1) / lmax;
+      if (np <= 1) {
+        vsegs.push_back(s);
+        continue;
+      }
+      const int64_t len = (s.ncol + np - 1) / np;
+      for (int64_t c = 0; c < s.ncol; c += len)
+        vsegs.push_back(SegDev{s.col0 + c, s.src0 + c, (int32_t)std::min<int64_t>(len, s.ncol - c), 0});
+    }
+  }
+  const std::vector<SegDev>& segs = vsegs;
+  const int nseg = (int)segs.size();
   const int64_t nrows = in.rows.nwin;
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -1108,7 +1130,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   // band of a task also computes the group's top edge (m terms per column).
   // Pick (G, bpt) minimising waves * task cost; G > 1 costs a merge pass.
   int64_t total_cols = 0;
-  for (const auto& s : in.segs) total_cols += s.ncol;
+  for (const auto& s : segs) total_cols += s.ncol;
   auto split = [&](int G, std::vector<int>& gs) {
     gs.assign(G + 1, nseg);
     gs[0] = 0;
@@ -1116,8 +1138,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     int64_t acc = 0;
     for (int g = 1; g < G; ++g) {
       const int64_t target = total_cols * g / G;
-      while (s < nseg - (G - g) && acc + in.segs[s].ncol <= target) acc += in.segs[s++].ncol;
-      if (s <= gs[g - 1]) acc += in.segs[s++].ncol;
+      while (s < nseg - (G - g) && acc + segs[s].ncol <= target) acc += segs[s++].ncol;
+      if (s <= gs[g - 1]) acc += segs[s++].ncol;
       gs[g] = s;
     }
   };
@@ -1130,7 +1152,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       int64_t cmax = 0, smax = 0;
       for (int q = 0; q < g; ++q) {
         int64_t c = 0;
-        for (int s = gs[q]; s < gs[q + 1]; ++s) c += in.segs[s].ncol;
+        for (int s = gs[q]; s < gs[q + 1]; ++s) c += segs[s].ncol;
         cmax = std::max(cmax, c);
         smax = std::max<int64_t>(smax, gs[q + 1] - gs[q]);
       }
@@ -1158,7 +1180,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     int64_t off = 0;
     for (int s = group_seg[g]; s < group_seg[g + 1]; ++s) {
       eoff[s] = (int)off;
-      off += (in.segs[s].ncol + 1) & ~1;
+      off += (segs[s].ncol + 1) & ~1;
     }
     ecap = std::max(ecap, off);
   }
@@ -1186,7 +1208,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     if (err) *err = Error{kCudaError, "device allocation failed for the join"};
     return kCudaError;
   }
-  CUDA_TRY(cudaMemcpyAsync(d_segs, in.segs.data(), sizeof(SegDev) * nseg, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d_segs, segs.data(), sizeof(SegDev) * nseg, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(d_eoff, eoff.data(), sizeof(int) * nseg, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(d_gs, group_seg.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice, st));
   int nl = 0;
@@ -1216,7 +1238,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
         if (in.ev[0]) CUDA_TRY(cudaEventRecord(in.ev[0], st));
         in.heads_used = true;
         const int rc = compute_heads_fft(in.xa, in.na, nrows, hstride, in.rows.mu, in.rows.flag, d_btil, d_ebt,
-                                         d_col, d_segs, nseg, m, d_heads, hstride, d_seed, arena, st, &nl, err);
+                                         d_col, d_segs, nseg, m, d_heads, hstride, d_seed, SELF ? in.excl : -1,
+                                         arena, st, &nl, err);
         if (rc != kOk) return rc;
         if (in.ev[1]) CUDA_TRY(cudaEventRecord(in.ev[1], st));
       }

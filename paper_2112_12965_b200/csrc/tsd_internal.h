@@ -119,11 +119,13 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
 // 4096-point transform with >= 512 rows per block.
 int heads_fft_supported(int m);
 // d_seed (optional, nrows): per row the order-preserving u64 key of its best
-// column-0 candidate max_s head * kf over ALL segments (0 = none); one ulp
-// below it is a strict lower bound the join starts from (join.cu, k_join).
+// admissible column-0 candidate max_s head * invn_b over ALL segments (0 =
+// none; excl >= 0: self-join, heads inside the exclusion zone skipped); one
+// ulp below it is a strict lower bound the join starts from (k_join).
 int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrows, const double* d_mua,
                       const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
-                      unsigned long long* d_seed, Arena& arena, cudaStream_t st, int* launches, Error* err);
+                      unsigned long long* d_seed, long long excl, Arena& arena, cudaStream_t st, int* launches,
+                      Error* err);
 
 // Epilogue: corr -> distance (series.hpp:153-161), concat column -> source
 // coordinate (dictionary.hpp:183-188), (inf, -1) sentinel for rows without an

@@ -143,6 +143,35 @@ def test_self_join_exclusion_parameter_ecg(excl):
     check_profile(P.values, P.indices, rv, ri, m, ab_dist(t, t, m), label=f"self excl={excl}")
 
 
+def test_self_join_large_sampled_rows_virtual_segments():
+    """n = 2^18 self-join (one long segment cut into virtual column pieces,
+    several segment groups, exclusion-aware head seeds) and a 2^16 x 2^18
+    AB-join: sampled rows against the oracle, each row's admissible set
+    restated as a two-segment dictionary around its exclusion zone."""
+    n, m = 1 << 18, 256
+    t = synth.walk(51, n)
+    P = tsd.self_join(t, m)
+    excl = m // 2
+    cnt = n - m + 1
+    rng = np.random.default_rng(5)
+    rows = np.concatenate([[0, 1, excl, cnt // 2, cnt - 1], rng.choice(cnt, 19, replace=False)])
+    for i in rows:
+        segs, starts = [], []
+        if i - excl - 1 >= 0:  # windows 0 .. i-excl-1
+            segs.append(t[: i - excl - 1 + m]); starts.append(0)
+        if i + excl + 1 <= cnt - 1:  # windows i+excl+1 .. cnt-1
+            segs.append(t[i + excl + 1:]); starts.append(i + excl + 1)
+        rv, ri = O.dict_join(t[i:i + m], segs, starts, m)
+        check_profile(P.values[i:i + 1], P.indices[i:i + 1], rv, ri, m, dict_dist(t[i:i + m], segs, starts, m),
+                      label=f"self n=2^18 row {i}")
+    a = synth.walk(52, 1 << 16)
+    Q = tsd.ab_join(a, t, m)
+    for i in rng.choice((1 << 16) - m + 1, 16, replace=False):
+        rv, ri = O.ab_join(a[i:i + m], t, m)
+        check_profile(Q.values[i:i + 1], Q.indices[i:i + 1], rv, ri, m, ab_dist(a[i:i + m], t, m),
+                      label=f"ab 2^16 x 2^18 row {i}")
+
+
 def test_flat_windows_ab_and_self():
     """flat stretches in query and target (profiles.hpp:290-294, :331-336)"""
     a = synth.Rng(9).noise(2000)
