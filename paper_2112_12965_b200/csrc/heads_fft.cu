@@ -230,11 +230,20 @@ struct HeadsArgs {
   const double4* col;     // FP64 packed column data (.z = invn_b), read for the seeds
   const uint8_t* flag_a;  // row flags (bit0 valid, bit1 flat)
   int nseg, npairs, m, Q;
-  long long excl;  // self-join exclusion half-width (-1: AB join); a seed candidate needs |i - col0| > excl
+  long long excl;  // self-join exclusion half-width (-1: AB join)
+  int sym;         // symmetric self-join: a row's sweep evaluates only its upper-triangle heads
   double* heads;
   unsigned long long* seed;  // per row: order-preserving key of max_s head * kf (0 = none), or null
   int ppc;                   // pairs per CTA
 };
+
+// A head (row i, column c) may seed row i only if row i's own sweep evaluates
+// that very cell from the same head value: every admissible column (|i - c| >
+// excl) in the AB / full self-join sweeps, only upper ones (c - i > excl) in
+// the symmetric sweep (a lower cell is evaluated by the column side through the
+// recurrence, whose rounding differs from the FFT head's).
+struct HeadsArgs;
+__device__ __forceinline__ bool seed_ok(const HeadsArgs& a, long long i, long long c);
 
 // order-preserving map double -> u64 (key(a) < key(b) iff a < b; 0 below all)
 __device__ __forceinline__ unsigned long long order_key(double v) {
@@ -251,6 +260,11 @@ __device__ __forceinline__ void cp16(void* sdst, const void* gsrc) {
 // half twiddle table | per-row mean offsets. Thread j only ever touches
 // spectrum / offset entries j + 256 r, so those need no barriers.
 constexpr size_t HEADS_SMEM = sizeof(double2) * (FFT_PAD + FFT_N + FFT_N / 2) + sizeof(double) * FFT_N;
+
+__device__ __forceinline__ bool seed_ok(const HeadsArgs& a, long long i, long long c) {
+  if (a.excl < 0) return true;
+  return c - i > a.excl || (!a.sym && i - c > a.excl);
+}
 
 __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
   extern __shared__ double2 fsm[];
@@ -303,11 +317,11 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
         const double d = dmu[q];
         const double g0 = v[r].x * invN - d * e0;
         h0[i] = g0;
-        if (a.excl < 0 || i - c0 > a.excl || c0 - i > a.excl) mk[r] = fmax(mk[r], g0 * k0);
+        if (seed_ok(a, i, c0)) mk[r] = fmax(mk[r], g0 * k0);
         if (two) {
           const double g1 = v[r].y * invN - d * e1;
           h1[i] = g1;
-          if (a.excl < 0 || i - c1 > a.excl || c1 - i > a.excl) mk[r] = fmax(mk[r], g1 * k1);
+          if (seed_ok(a, i, c1)) mk[r] = fmax(mk[r], g1 * k1);
         }
       }
     }
@@ -328,8 +342,8 @@ int heads_fft_supported(int m) { return m >= 1 && m <= FFT_N - 512 + 1; }
 
 int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrows, const double* d_mua,
                       const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
-                      unsigned long long* d_seed, long long excl, Arena& arena, cudaStream_t st, int* launches,
-                      Error* err) {
+                      unsigned long long* d_seed, long long excl, int sym, Arena& arena, cudaStream_t st,
+                      int* launches, Error* err) {
   const int npairs = (nseg + 1) / 2;
   double2* d_tw = (double2*)arena.get(sizeof(double2) * FFT_N);
   double2* d_spec = (double2*)arena.get(sizeof(double2) * FFT_N * (size_t)npairs);
@@ -363,6 +377,7 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
   a.heads = d_heads;
   a.seed = d_seed;
   a.excl = excl;
+  a.sym = sym;
   a.ppc = 16;
   if (d_seed) CUDA_TRY(cudaMemsetAsync(d_seed, 0, sizeof(unsigned long long) * nrows, st));
   const int64_t nblk = (hrows + a.Q - 1) / a.Q;

@@ -31,6 +31,7 @@
 //     Flat rows (invn_a == 0) are resolved in the epilogue from the flat
 //     column table (profiles.hpp:332-336 gives them c in {0, 1}).
 #include <algorithm>
+#include <queue>
 #include <cfloat>
 #include <climits>
 #include <cstdio>
@@ -92,13 +93,19 @@ struct JoinArgs {
   const unsigned long long* seed;  // per-row order key of the best head candidate (heads_fft.cu), or null
   double* out_c;  // [ngroups][nrows]
   int64_t* out_j;
+  // symmetric self-join (SYM kernels): task queue and the column side
+  const int4* tasks;             // {band0, band1, group, 0}, longest first
+  int* task_next;                // dynamic task counter
+  unsigned long long* ccand;     // [SYM_NC][ccols]: {order key of corr, row index} (16 B, 128-bit CAS)
+  int64_t ccols;                 // columns per ccand copy
+  double* cthr;                  // per column: kplus(best corr) * norm_b * (1 - 2^-40)
 };
 
 template <int R>
 struct __align__(16) WarpSmem {
   double4 colbuf[3][32];
   double ering[96];
-  double edummy[96];  // lanes 0..30 store here so lane 31's edge store needs no branch
+  double cring[96];   // SYM: column thresholds (cthr snapshot), same ring layout as ering
   double bK[R][32];  // best K = cov * invn_b per slot (row factor invn_a left out); +inf = inactive row
   int bj[R][32];     // its concatenated column
   double slide[Geo<R>::SLIDE];
@@ -106,7 +113,7 @@ struct __align__(16) WarpSmem {
 };
 
 #ifdef TSD_COUNT_EXACT
-__device__ unsigned long long g_exact_count, g_step_count, g_exact_first, g_step_first;
+__device__ unsigned long long g_exact_count, g_step_count, g_exact_first, g_step_first, g_col_count, g_cas_count;
 #endif
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -274,6 +281,8 @@ struct SweepCtx {
   long long excl;  // self-join exclusion half-width
   bool write_out;
   bool first_seg;  // diagnostics only
+  const double* cthr;  // SYM: column thresholds of this segment (col0 aligned)
+  double namin;        // SYM: (smallest row norm among this lane's slots)
 };
 
 // chunk c of the segment: column data for steps [32c, 32c+32) -> colbuf[c%3],
@@ -285,6 +294,7 @@ __device__ __forceinline__ void issue_chunk(WarpSmem<R>& sm, const SweepCtx& cx,
   cp16(dst, src);
   cp16(reinterpret_cast<char*>(dst) + 16, reinterpret_cast<const char*>(src) + 16);
   if (lane < 16) cp16(&sm.ering[(c % 3) * 32 + 2 * lane], cx.E + 32 * c + 2 * lane);
+  else if (cx.cthr) cp16(&sm.cring[(c % 3) * 32 + 2 * (lane - 16)], cx.cthr + 32 * c + 2 * (lane - 16));
   cp_commit();
 }
 
@@ -292,6 +302,119 @@ template <int R>
 __device__ __forceinline__ void flush_block(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int b) {
   const int j = 32 * b + lane;
   if (j < cx.ncol - 1) cx.E[j] = sm.ering[(b % 3) * 32 + lane];
+}
+
+// ---------------------------------------------------------------------------
+// Symmetric self-join, column side. The reference walks each admissible
+// unordered pair once and updates both rows (profiles.hpp:287-297). A band
+// here sweeps only columns j > i + excl (upper triangle); besides its own
+// rows (row side, as in the AB join) every cell is a candidate for row j's
+// profile -- the column side. Per step the warp tests all 8 x 32 cells of
+// column j against one threshold: corr = cov * invn_a * invn_b > best_j
+// implies cov > best_j * norm_b[j] * min(norm_a over the lane's rows), i.e.
+// hi(cov) >= hi(cthr[j] * namin) with cthr[j] = kplus(best_j) * norm_b[j] *
+// (1 - 2^-40) staged per chunk. A pass reduces the warp's best (corr, row)
+// (max corr, lowest row) and merges it into ccand[j] with a 128-bit CAS.
+__device__ __forceinline__ double kplus_d(double b) { return b > 0.0 ? b : -0.0; }
+// SYM column candidates are spread over SYM_NC copies (by task) so that the
+// many bands sweeping the same columns at once do not serialise on one CAS
+// target; the copies are merged per row after the join
+constexpr int SYM_NC = 16;
+__device__ __forceinline__ unsigned long long order_key(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double key_value(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+__device__ __forceinline__ void cas128(unsigned long long* p, unsigned long long clo, unsigned long long chi,
+                                       unsigned long long nlo, unsigned long long nhi, unsigned long long& olo,
+                                       unsigned long long& ohi) {
+  asm volatile(
+      "{\n .reg .b128 d, c, s;\n mov.b128 c, {%2, %3};\n mov.b128 s, {%4, %5};\n"
+      " atom.global.cas.b128 d, [%6], c, s;\n mov.b128 {%0, %1}, d;\n}\n"
+      : "=l"(olo), "=l"(ohi)
+      : "l"(clo), "l"(chi), "l"(nlo), "l"(nhi), "l"(p)
+      : "memory");
+}
+
+// vals: the lane's 8 slot covariances at column col (shared memory [8][32]);
+// cm: slots that passed the column threshold. The warp's lexicographic best (max corr, lowest row) is found
+// with three REDUX reductions on the order key and the row.
+__device__ __noinline__ void col_update(const double* vals, const double* __restrict__ invn_a, int lane,
+                                        unsigned cm, long long row0, long long col, double invb, long long excl,
+                                        long long nrows, unsigned long long* ccand, double* cthr) {
+  unsigned long long bk = 0;  // order key of the lane's best corr (0 = none)
+  unsigned brow = 0xffffffffu;
+  if (invb > 0.0) {
+    for (unsigned mm = cm; mm; mm &= mm - 1) {
+      const int r = __ffs(mm) - 1;
+      const long long row = row0 + r;
+      const long long d = col - row;
+      const double ia = row < nrows ? invn_a[row] : 0.0;
+      if ((d > excl || d < -excl) && ia > 0.0) {
+        const double c = clamp_corr(vals[r * 32 + lane] * ia * invb);  // profiles.hpp:289-294
+        const unsigned long long k = order_key(c);
+        if (k > bk || (k == bk && (unsigned)row < brow)) {
+          bk = k;
+          brow = (unsigned)row;
+        }
+      }
+    }
+  }
+  const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(bk >> 32));
+  const unsigned lo = __reduce_max_sync(0xffffffffu, (unsigned)(bk >> 32) == hi ? (unsigned)bk : 0u);
+  const unsigned long long wk = ((unsigned long long)hi << 32) | lo;
+  const unsigned wrow = __reduce_min_sync(0xffffffffu, bk == wk ? brow : 0xffffffffu);
+#ifdef TSD_COUNT_EXACT
+  if (lane == 0) atomicAdd(&g_col_count, 1ull);
+  if (lane == 0 && wk != 0) atomicAdd(&g_cas_count, 1ull);
+#endif
+  if (lane == 0 && wk != 0) {
+    unsigned long long* p = ccand + 2 * col;
+    const unsigned long long nk = wk, ni = (unsigned long long)wrow;
+    unsigned long long ck = p[0], ci = p[1];  // may be torn: the CAS validates
+    while (nk > ck || (nk == ck && ni < ci)) {
+      unsigned long long ok, oi;
+      cas128(p, ck, ci, nk, ni, ok, oi);
+      if (ok == ck && oi == ci) {
+        const double t = kplus_d(key_value(nk)) * (1.0 / invb) * (1.0 - 0x1p-40);
+        atomicMax(reinterpret_cast<long long*>(cthr + col), __double_as_longlong(t));
+        break;
+      }
+      ck = ok;
+      ci = oi;
+    }
+  }
+}
+
+// SYM exact update, shared by every unrolled step (one copy of the code keeps
+// the sweep loop inside the instruction cache). vals: the lane's 8 slot
+// covariances in logical slot order (shared memory [8][32]). Row side as in
+// sweep_block; column side via col_update. Returns the lane's mask of slots
+// whose best changed (the caller refreshes their thresholds).
+template <int R>
+__device__ __noinline__ unsigned exact_update_sym(WarpSmem<R>& sm, int lane, long long col, double invb, int tc,
+                                                  long long row0, long long excl, const double* __restrict__ invn_a,
+                                                  long long nrows, unsigned long long* ccand, double* cthr) {
+  const double* vals = sm.slide;
+  unsigned upd = 0, cm = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const double v = vals[r * 32 + lane];
+    const double K = v * invb;
+    const long long d = row0 + r - col;
+    if (K > sm.bK[r][lane] && (d > excl || d < -excl)) {  // profiles.hpp:70-77, :281-284
+      sm.bK[r][lane] = K;
+      sm.bj[r][lane] = (int)col;
+      upd |= 1u << r;
+    }
+    cm |= (__double2hiint(v) >= tc ? 1u : 0u) << r;
+  }
+  if (__any_sync(0xffffffffu, cm != 0))
+    col_update(vals, invn_a, lane, cm, row0, col, invb, excl, nrows, ccand, cthr);
+  return upd;
 }
 
 // FP64 sweep: the unnormalised centred recurrence of the reference
@@ -348,10 +471,11 @@ struct SweepState {
 // run past ncol. Ring/colbuf positions are resolved once per block: E[k0 ..
 // k0+R-1] are contiguous, only E[k0-1] may sit in the previous ring block,
 // and only step k0+R's column data in the next chunk.
-template <int R, bool SELF, bool FIRST, bool GUARD>
+template <int R, bool SELF, bool FIRST, bool GUARD, bool SYM>
 __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int k0, int m96,
                                             SweepState<R>& S, const double (&dfa)[R], const double (&dga)[R],
-                                            double* sbase, bool l0) {
+                                            double* sbase, bool l0, const double* __restrict__ invn_a,
+                                            long long nrows, unsigned long long* ccand, double* cthr) {
   // colbuf and the edge ring are both 96-entry rings indexed by column mod 96
   const int n = cx.ncol;
   const double4* cflat = &sm.colbuf[0][0];
@@ -361,6 +485,7 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
   double* const st_prev = sbase + (m96 == 0 ? 95 : m96 - 1);  // E[k0-1]
   double* const st_cur = sbase + ebase;
   double nmin = 0.0;
+  int tcb = INT_MAX;  // SYM: column threshold of the current threshold block
 #pragma unroll
   for (int u = 0; u < R; ++u) {
     const int k = k0 + u;
@@ -368,8 +493,15 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
     const int ph = (R - u) & (R - 1);  // physical register of slot 0 at this step
     if (u % TB == 0) {  // threshold block of TB columns (nmin prefetched with its first column)
       nmin = (FIRST && u == 0) ? ccur[0].w : S.nx.nmin;
+      if (SYM) {  // column side folded in: the block's weakest column threshold
+        double cmin = sm.cring[ebase + u];
 #pragma unroll
-      for (int r = 0; r < R; ++r) S.thr[r] = __double2hiint(S.bKp[r] * nmin);
+        for (int t = 1; t < TB; ++t) cmin = fmin(cmin, sm.cring[ebase + u + t]);
+        tcb = __double2hiint(cmin * cx.namin);
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) S.thr[r] = SYM ? min(__double2hiint(S.bKp[r] * nmin), tcb)
+                                                  : __double2hiint(S.bKp[r] * nmin);
     }
     if (!(FIRST && u == 0)) {
       // fold in the incoming diagonal; lane 31 retires its bottom-row value (column k-1)
@@ -399,6 +531,23 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
       // invn_b = 0 -> K = 0 (profiles.hpp:332-336)
       const double invb = ccur[u].z;
       const int col = cx.colbase + k;
+      if constexpr (SYM) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm.slide[r * 32 + lane] = S.P[(r + ph) & (R - 1)];
+        __syncwarp();
+        const int tc = __double2hiint(sm.cring[ebase + u] * cx.namin);  // this column's own threshold
+        const unsigned upd =
+            exact_update_sym<R>(sm, lane, col, invb, tc, cx.row0, cx.excl, invn_a, nrows, ccand, cthr);
+        __syncwarp();
+        if (upd) {
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+            if ((upd >> r) & 1u) {
+              S.bKp[r] = kplus(sm.bK[r][lane]);
+              S.thr[r] = min(__double2hiint(S.bKp[r] * nmin), tcb);
+            }
+        }
+      } else {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double K = S.P[(r + ph) & (R - 1)] * invb;
@@ -414,6 +563,7 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
           S.thr[r] = __double2hiint(S.bKp[r] * nmin);
         }
       }
+      }
     }
   }
 }
@@ -422,13 +572,16 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
 // diagonal, 2 DFMA per slot, prefetch the next step's column data / edge /
 // shuffle, K = cov * invn_b, the high-word test of every slot against its
 // threshold and one warp vote; the exact update runs only on a pass.
-template <int R, bool SELF>
+template <int R, bool SELF, bool SYM>
 __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, const double (&dfa)[R],
-                              const double (&dga)[R], SweepState<R>& S) {
+                              const double (&dga)[R], SweepState<R>& S, const double* __restrict__ invn_a,
+                              long long nrows, unsigned long long* ccand, double* cthr) {
   static_assert(R == 8, "the sweep is written for R = 8 rows per lane");
   const int n = cx.ncol;
   const int nchunks = (n + 31) >> 5;
-  double* const sbase = lane == 31 ? sm.ering : sm.edummy;  // lane 31 stores into the ring
+  // lane 31 stores the bottom row into the ring; lanes 0..30 into scratch
+  // (sm.slide[256..351], unused while sweeping) so the store needs no branch
+  double* const sbase = lane == 31 ? sm.ering : sm.slide + 256;
   const bool l0 = lane == 0;
   __syncwarp();
   issue_chunk(sm, cx, lane, 0);
@@ -454,19 +607,22 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   };
   constexpr int BPC = 32 / R;  // blocks per chunk
   if (n <= R) {
-    sweep_block<R, SELF, true, true>(sm, cx, lane, 0, 0, S, dfa, dga, sbase, l0);
+    sweep_block<R, SELF, true, true, SYM>(sm, cx, lane, 0, 0, S, dfa, dga, sbase, l0, invn_a, nrows, ccand, cthr);
   } else {
-    sweep_block<R, SELF, true, false>(sm, cx, lane, 0, 0, S, dfa, dga, sbase, l0);
+    sweep_block<R, SELF, true, false, SYM>(sm, cx, lane, 0, 0, S, dfa, dga, sbase, l0, invn_a, nrows, ccand, cthr);
     // the turn happens before the LAST block of a chunk: that block's final
     // step prefetches the first column of the next chunk
     int k0 = R, m96 = R, bic = 1;  // column, column mod 96, block index inside the chunk
     for (; k0 + R <= n; k0 += R) {
       if (bic == BPC - 1 && k0 + R < n) chunk_turn((k0 + R) >> 5);
-      sweep_block<R, SELF, false, false>(sm, cx, lane, k0, m96, S, dfa, dga, sbase, l0);
+      sweep_block<R, SELF, false, false, SYM>(sm, cx, lane, k0, m96, S, dfa, dga, sbase, l0, invn_a, nrows, ccand,
+                                             cthr);
       m96 = m96 + R == 96 ? 0 : m96 + R;
       bic = bic == BPC - 1 ? 0 : bic + 1;
     }
-    if (k0 < n) sweep_block<R, SELF, false, true>(sm, cx, lane, k0, m96, S, dfa, dga, sbase, l0);
+    if (k0 < n)
+      sweep_block<R, SELF, false, true, SYM>(sm, cx, lane, k0, m96, S, dfa, dga, sbase, l0, invn_a, nrows, ccand,
+                                             cthr);
   }
   cp_wait<0>();
   __syncwarp();
@@ -645,7 +801,7 @@ __device__ void sweep_segment32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, c
   constexpr int R = 8;
   const int n = cx.ncol;
   const int nchunks = (n + 31) >> 5;
-  float* const sbase = reinterpret_cast<float*>(lane == 31 ? sm.ering : sm.edummy);
+  float* const sbase = reinterpret_cast<float*>(lane == 31 ? sm.ering : sm.slide + 256);
   const bool l0 = lane == 0;
   __syncwarp();
   issue_chunk32(sm, cx, lane, 0);
@@ -690,8 +846,9 @@ __device__ void sweep_segment32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, c
   __syncwarp();
 }
 
-template <int R, bool SELF, bool F32>
+template <int R, bool SELF, bool F32, bool SYM>
 __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_MINB) k_join(const JoinArgs a) {
+  static_assert(!SYM || (SELF && !F32), "the symmetric sweep is the FP64 self-join");
   constexpr int H = Geo<R>::H;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpSmem<R>* smem = reinterpret_cast<WarpSmem<R>*>(smem_raw);
@@ -704,13 +861,34 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
   const int bpt = a.bands_per_task;
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
 
-  for (int task = gw; task < a.ntasks; task += nw) {
-    const int g = task % a.ngroups;
-    const int b0 = (task / a.ngroups) * bpt;
-    const int b1 = min(a.nbands, b0 + bpt);
+  for (int it = 0;; ++it) {
+    int task, g, b0, b1;
+    if constexpr (SYM) {  // triangle tasks differ in size: dynamic queue, longest first
+      if (lane == 0) task = atomicAdd(a.task_next, 1);
+      task = __shfl_sync(0xffffffffu, task, 0);
+      if (task >= a.ntasks) break;
+      const int4 t4 = a.tasks[task];
+      b0 = t4.x;
+      b1 = t4.y;
+      g = t4.z;
+    } else {
+      task = gw + it * nw;
+      if (task >= a.ntasks) break;
+      g = task % a.ngroups;
+      b0 = (task / a.ngroups) * bpt;
+      b1 = min(a.nbands, b0 + bpt);
+    }
     const int s_beg = a.group_seg[g], s_end = a.group_seg[g + 1];
     for (int b = b0; b < b1; ++b) {
       const int64_t i0 = (int64_t)b * H;
+      double namin = DBL_MAX;  // SYM: smallest window norm among this lane's rows
+      if constexpr (SYM) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int64_t i = i0 + R * lane + r;
+          if (i < a.nrows && a.flag_a[i] == 1) namin = fmin(namin, 1.0 / a.invn_a[i]);
+        }
+      }
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int64_t i = i0 + R * lane + r;
@@ -737,18 +915,47 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           }
         }
       }
+      if constexpr (SYM) {
+        // the column side may already hold a better lower bound for these rows
+        // (their lower-triangle pairs, deposited by earlier bands). For the
+        // self-join row i and column i are the same window, so cthr[i] =
+        // kplus(best corr) * norm_i * (1 - 2^-40) is that bound in the row's K
+        // units. Lower-triangle candidates have lower indices than any
+        // row-side one, so starting at it loses no tie.
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int64_t i = i0 + R * lane + r;
+          const double bk = sm.bK[r][lane];
+          if (i < a.nrows && bk != kInf) {
+            const double klb = a.cthr[i];
+            if (klb > bk) sm.bK[r][lane] = klb;
+          }
+        }
+      }
       const double cA = a.mua[i0];
       for (int s = s_beg; s < s_end; ++s) {
-        const SegDev sg = a.segs[s];
+        const SegDev sg0 = a.segs[s];
+        // SYM: the band sweeps only columns from its first admissible one on
+        // (aligned down to 32; the cells before the staircase are masked)
+        int q = 0;
+        if constexpr (SYM) {
+          const int64_t d = i0 + a.excl + 1 - sg0.col0;
+          const int64_t qa = d & ~int64_t(31);
+          q = d <= 0 ? 0 : (int)(qa < (int64_t)sg0.ncol ? qa : (int64_t)sg0.ncol);
+          if (q >= sg0.ncol) continue;
+        }
+        const SegDev sg{sg0.col0 + q, sg0.src0 + q, sg0.ncol - q, 0};
         SweepCtx cx;
         cx.colg = a.col + sg.col0;
-        cx.E = Ew + a.seg_eoff[s];
+        cx.E = Ew + a.seg_eoff[s] + q;
         cx.ncol = sg.ncol;
         cx.colbase = (int)sg.col0;
         cx.write_out = (b + 1 < b1);
         cx.row0 = i0 + R * lane;
         cx.excl = a.excl;
         cx.first_seg = (s == s_beg);
+        cx.cthr = SYM ? a.cthr + sg.col0 : nullptr;
+        cx.namin = namin;
         if (b == b0 && sg.ncol >= 2) {
           // top edge of the task: E[j] = cov(re, j + delta), j = 0 .. ncol-2
           // (row 0 has df = dg = 0, so E[j] = cov(0, j+1) feeds it exactly)
@@ -780,7 +987,16 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           __syncwarp();
         }
         double head[R];
-        if (a.heads) {  // left edge precomputed by FFT correlation (heads_fft.cu)
+        if (SYM && q > 0) {  // left edge at an interior column of the piece: direct dot products
+          double out[R], eU;
+          sliding_dot<R>(sm, a.xb + sg.col0, a.mub[sg.col0], a.xa + i0, a.na - i0, cA, a.m, lane, out, &eU);
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int64_t i = i0 + R * lane + r;
+            const double mu = i < a.nrows ? a.mua[i] : cA;
+            head[r] = out[r] - (mu - cA) * eU;
+          }
+        } else if (a.heads) {  // left edge precomputed by FFT correlation (heads_fft.cu)
           const double2* hp = reinterpret_cast<const double2*>(a.heads + s * a.hstride + i0 + R * lane);
 #pragma unroll
           for (int r = 0; r < R / 2; ++r) {
@@ -862,7 +1078,8 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
             dga[r] = in ? a.dga[i] : 0.0;
             S.bKp[r] = kplus(sm.bK[r][lane]);
           }
-          sweep_segment<R, SELF>(sm, cx, lane, dfa, dga, S);
+          sweep_segment<R, SELF, SYM>(sm, cx, lane, dfa, dga, S, a.invn_a, a.nrows,
+                                      SYM ? a.ccand + (int64_t)(task % SYM_NC) * 2 * a.ccols : nullptr, a.cthr);
         }
       }
       // band results: c = clamp(K * invn_a) (profiles.hpp:331, :335)
@@ -1083,7 +1300,63 @@ __global__ void k_epilogue(const double* __restrict__ bc, const int64_t* __restr
 
 namespace {
 
-template <int R, bool SELF, bool F32>
+// SYM: per row, the lexicographic best of the row side (per-group partials)
+// and the column side (ccand) -- acc_merge's rule (profiles.hpp:63-85)
+__global__ void k_merge_sym(const double* __restrict__ pc, const int64_t* __restrict__ pj, int64_t nrows, int ngroups,
+                            const unsigned long long* __restrict__ ccand, int64_t nrows_cols, double* __restrict__ oc,
+                            int64_t* __restrict__ oj) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nrows) return;
+  double bc = -2.0;
+  int64_t bj = -1;
+  for (int g = 0; g < ngroups; ++g) {
+    const double cc = pc[(int64_t)g * nrows + i];
+    const int64_t jj = pj[(int64_t)g * nrows + i];
+    if (jj >= 0 && (bj < 0 || better(cc, jj, bc, bj))) {
+      bc = cc;
+      bj = jj;
+    }
+  }
+  for (int c = 0; c < SYM_NC; ++c) {
+    const unsigned long long* q = ccand + (int64_t)c * 2 * nrows_cols + 2 * i;
+    const unsigned long long ci = q[1];
+    if (ci != ~0ull) {
+      const double cc = key_value(q[0]);
+      const int64_t jj = (int64_t)ci;
+      if (bj < 0 || better(cc, jj, bc, bj)) {
+        bc = cc;
+        bj = jj;
+      }
+    }
+  }
+  oc[i] = bj >= 0 ? bc : -2.0;
+  oj[i] = bj;
+}
+
+// SYM: column side initial state from the row seeds (a lower bound of each
+// row's final best, never reported: index "none" = ~0)
+__global__ void k_sym_init(const unsigned long long* __restrict__ seed, const double* __restrict__ invn,
+                           const uint8_t* __restrict__ flag, int64_t n, unsigned long long* __restrict__ ccand,
+                           double* __restrict__ cthr) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n + 64) return;
+  if (j >= n) {
+    cthr[j] = DBL_MAX;
+    return;
+  }
+  double lb = -2.0;
+  const double iv = invn[j];
+  const bool act = flag[j] == 1 && iv > 0.0;
+  if (act && seed && seed[j] != 0ull) lb = nextafter(key_value(seed[j]), -DBL_MAX) * iv * (1.0 - 0x1p-40);
+  for (int c = 0; c < SYM_NC; ++c) {
+    ccand[(int64_t)c * 2 * n + 2 * j] = order_key(lb);
+    ccand[(int64_t)c * 2 * n + 2 * j + 1] = ~0ull;
+  }
+  // flat / inactive rows: resolved by the epilogue; their column side never triggers
+  cthr[j] = act ? kplus_d(lb) * (1.0 / iv) * (1.0 - 0x1p-40) : DBL_MAX;
+}
+
+template <int R, bool SELF, bool F32, bool SYM>
 int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st, Error* err,
                 int* launches) {
   constexpr int H = Geo<R>::H;
@@ -1104,7 +1377,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
         vsegs.push_back(s);
         continue;
       }
-      const int64_t len = (s.ncol + np - 1) / np;
+      const int64_t len = (((s.ncol + np - 1) / np) + 31) & ~int64_t(31);  // pieces start 32-aligned
       for (int64_t c = 0; c < s.ncol; c += len)
         vsegs.push_back(SegDev{s.col0 + c, s.src0 + c, (int32_t)std::min<int64_t>(len, s.ncol - c), 0});
     }
@@ -1116,7 +1389,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem_bytes = sizeof(WarpSmem<R>) * WARPS;
-  auto kern = k_join<R, SELF, F32>;
+  auto kern = k_join<R, SELF, F32, SYM>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * WARPS, smem_bytes);
@@ -1172,8 +1445,57 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       }
     }
   }
+  // SYM: one group per piece; bands sweep only their triangle part, so task
+  // sizes differ -- choose bpt by an LPT (longest first onto the least-loaded
+  // warp) makespan estimate and hand tasks out dynamically in that order
+  std::vector<int4> sym_tasks;
+  if constexpr (SYM) {
+    G = nseg;
+    auto qoff = [&](int b, int sgi) -> int64_t {  // first swept local column (kernel: q)
+      const int64_t d = (int64_t)b * H + in.excl + 1 - segs[sgi].col0;
+      return d <= 0 ? 0 : std::min<int64_t>(d & ~int64_t(31), segs[sgi].ncol);
+    };
+    double best = 1e300;
+    int bbest = 1;
+    std::vector<std::pair<double, int4>> cand;
+    for (int bp = 1; bp <= std::min(nbands, 1024); bp *= 2) {
+      cand.clear();
+      for (int b0 = 0; b0 < nbands; b0 += bp) {
+        const int b1 = std::min(nbands, b0 + bp);
+        for (int g = 0; g < G; ++g) {
+          double c = 0.0;
+          for (int b = b0; b < b1; ++b) c += (double)H * 2.5 * (double)(segs[g].ncol - qoff(b, g));
+          if (c <= 0.0) continue;
+          c += (double)(segs[g].ncol - qoff(b0, g)) * m + (double)H * m;  // top edge + head
+          cand.push_back({c, make_int4(b0, b1, g, 0)});
+        }
+      }
+      std::sort(cand.begin(), cand.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+      std::priority_queue<double, std::vector<double>, std::greater<double>> load;
+      for (int w = 0; w < nwarps; ++w) load.push(0.0);
+      double mk = 0.0;
+      for (const auto& c : cand) {
+        const double l = load.top() + c.first;
+        load.pop();
+        load.push(l);
+        mk = std::max(mk, l);
+      }
+      if (mk < best * 0.999) {
+        best = mk;
+        bbest = bp;
+        sym_tasks.clear();
+        for (const auto& c : cand) sym_tasks.push_back(c.second);
+      }
+    }
+    bpt = bbest;
+  }
   std::vector<int> group_seg;
-  split(G, group_seg);
+  if (SYM) {
+    group_seg.resize(nseg + 1);
+    for (int g = 0; g <= nseg; ++g) group_seg[g] = g;
+  } else {
+    split(G, group_seg);
+  }
   std::vector<int> eoff(nseg);
   int64_t ecap = 0;
   for (int g = 0; g < G; ++g) {
@@ -1186,7 +1508,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   }
   ecap = (ecap + 64 + 31) & ~int64_t(31);
   const int nbr = (nbands + bpt - 1) / bpt;
-  const int ntasks = nbr * G;
+  const int ntasks = SYM ? (int)sym_tasks.size() : nbr * G;
   const int grid = std::max(1, std::min(nsm * occ, (ntasks + WARPS - 1) / WARPS));
   const int used_warps = grid * WARPS;
   if (getenv("TSD_VERBOSE"))
@@ -1202,8 +1524,30 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   double* d_ebt = (double*)arena.get(sizeof(double) * nseg);
   double* d_edges = (double*)arena.get(sizeof(double) * ecap * used_warps);
   double* d_hscr = (double*)arena.get(sizeof(double) * 2048 * used_warps);
-  double* d_pc = G > 1 ? (double*)arena.get(sizeof(double) * nrows * G) : d_best_c;
-  int64_t* d_pj = G > 1 ? (int64_t*)arena.get(sizeof(int64_t) * nrows * G) : d_best_j;
+  const bool part = G > 1 || SYM;  // per-group partial outputs, merged afterwards
+  double* d_pc = part ? (double*)arena.get(sizeof(double) * nrows * G) : d_best_c;
+  int64_t* d_pj = part ? (int64_t*)arena.get(sizeof(int64_t) * nrows * G) : d_best_j;
+  int4* d_tasks = nullptr;
+  int* d_tnext = nullptr;
+  unsigned long long* d_ccand = nullptr;
+  double* d_cthr = nullptr;
+  if (SYM) {
+    d_tasks = (int4*)arena.get(sizeof(int4) * std::max<size_t>(1, sym_tasks.size()));
+    d_tnext = (int*)arena.get(sizeof(int));
+    d_ccand = (unsigned long long*)arena.get(sizeof(unsigned long long) * 2 * SYM_NC * (in.cols.nwin + 64));
+    d_cthr = (double*)arena.get(sizeof(double) * (in.cols.nwin + 64));
+    if (!d_tasks || !d_tnext || !d_ccand || !d_cthr) {
+      if (err) *err = Error{kCudaError, "device allocation failed for the symmetric self-join"};
+      return kCudaError;
+    }
+    if (!sym_tasks.empty())
+      CUDA_TRY(cudaMemcpyAsync(d_tasks, sym_tasks.data(), sizeof(int4) * sym_tasks.size(), cudaMemcpyHostToDevice,
+                               st));
+    CUDA_TRY(cudaMemsetAsync(d_tnext, 0, sizeof(int), st));
+    // (band range, group) pairs without columns are never queued: their
+    // partial rows must read "no candidate" in the merge
+    CUDA_TRY(cudaMemsetAsync(d_pj, 0xff, sizeof(int64_t) * nrows * G, st));
+  }
   if (!d_segs || !d_eoff || !d_gs || !d_col || !d_scale || !d_hscr || !d_btil || !d_ebt || !d_edges || !d_pc || !d_pj) {
     if (err) *err = Error{kCudaError, "device allocation failed for the join"};
     return kCudaError;
@@ -1239,7 +1583,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
         in.heads_used = true;
         const int rc = compute_heads_fft(in.xa, in.na, nrows, hstride, in.rows.mu, in.rows.flag, d_btil, d_ebt,
                                          d_col, d_segs, nseg, m, d_heads, hstride, d_seed, SELF ? in.excl : -1,
-                                         arena, st, &nl, err);
+                                         SYM ? 1 : 0, arena, st, &nl, err);
         if (rc != kOk) return rc;
         if (in.ev[1]) CUDA_TRY(cudaEventRecord(in.ev[1], st));
       }
@@ -1274,11 +1618,22 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   a.hscr = d_hscr;
   {
     const char* e = getenv("TSD_DMMA_HEADS");
-    a.dmma_heads = e ? atoi(e) : 1;
+    a.dmma_heads = SYM ? 0 : (e ? atoi(e) : 1);  // SYM heads sit at band-dependent columns
   }
   a.heads = d_heads;
   a.hstride = hstride;
   a.seed = d_heads ? d_seed : nullptr;
+  a.tasks = d_tasks;
+  a.task_next = d_tnext;
+  a.ccand = d_ccand;
+  a.ccols = in.cols.nwin;
+  a.cthr = d_cthr;
+  if (SYM) {
+    const int64_t nc = in.cols.nwin;
+    k_sym_init<<<(unsigned)((nc + 64 + 255) / 256), 256, 0, st>>>(a.seed, in.rows.invn, in.rows.flag, nc, d_ccand,
+                                                                  d_cthr);
+    ++nl;
+  }
   a.out_c = d_pc;
   a.out_j = d_pj;
 #ifdef TSD_COUNT_EXACT
@@ -1287,6 +1642,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   cudaMemcpyToSymbol(g_step_count, &zero, 8);
   cudaMemcpyToSymbol(g_exact_first, &zero, 8);
   cudaMemcpyToSymbol(g_step_first, &zero, 8);
+  cudaMemcpyToSymbol(g_col_count, &zero, 8);
+  cudaMemcpyToSymbol(g_cas_count, &zero, 8);
 #endif
   if (in.ev[2]) CUDA_TRY(cudaEventRecord(in.ev[2], st));
   kern<<<grid, 32 * WARPS, smem_bytes, st>>>(a);
@@ -1304,9 +1661,18 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     fprintf(stderr, "[tsd] exact-path steps %llu of %llu warp-steps (%.2f%%); first segment %.2f%%, others %.2f%%\n",
             ce, cs, 100.0 * ce / (cs ? cs : 1), 100.0 * cef / (csf ? csf : 1),
             100.0 * (ce - cef) / ((cs - csf) ? (cs - csf) : 1));
+    unsigned long long cc = 0, ca = 0;
+    cudaMemcpyFromSymbol(&cc, g_col_count, 8);
+    cudaMemcpyFromSymbol(&ca, g_cas_count, 8);
+    fprintf(stderr, "[tsd] column-side updates %llu (%.2f%% of warp-steps), with a candidate %llu\n", cc,
+            100.0 * cc / (cs ? cs : 1), ca);
   }
 #endif
-  if (G > 1) {
+  if (SYM) {
+    k_merge_sym<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(d_pc, d_pj, nrows, G, d_ccand, in.cols.nwin,
+                                                                  d_best_c, d_best_j);
+    ++nl;
+  } else if (G > 1) {
     k_merge_groups<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(d_pc, d_pj, nrows, G);
     ++nl;
     CUDA_TRY(cudaMemcpyAsync(d_best_c, d_pc, sizeof(double) * nrows, cudaMemcpyDeviceToDevice, st));
@@ -1346,8 +1712,8 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
              int* launches) {
   const bool self = in.excl >= 0;
   if (in.precision == 1) {
-    const int rc = self ? launch_join<8, true, true>(in, d_best_c, d_best_j, arena, st, err, launches)
-                        : launch_join<8, false, true>(in, d_best_c, d_best_j, arena, st, err, launches);
+    const int rc = self ? launch_join<8, true, true, false>(in, d_best_c, d_best_j, arena, st, err, launches)
+                        : launch_join<8, false, true, false>(in, d_best_c, d_best_j, arena, st, err, launches);
     if (rc != kOk) return rc;
     const int64_t n = in.rows.nwin;
     k_refine_fp64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_best_c, d_best_j, n, in.xa, in.rows.mu,
@@ -1361,8 +1727,19 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     }
     return kOk;
   }
-  return self ? launch_join<8, true, false>(in, d_best_c, d_best_j, arena, st, err, launches)
-              : launch_join<8, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
+  if (self) {
+    // The symmetric upper-triangle sweep evaluates each admissible pair once
+    // and updates both rows, as the reference does (profiles.hpp:287-297).
+    // Its column side needs the bests of earlier waves of bands to filter
+    // well, so it wins from ~450k windows (several waves on 148 SMs); below
+    // that the full-matrix sweep (every pair from both rows) is faster.
+    // TSD_SYM=1 / 0 forces either.
+    const char* e = getenv("TSD_SYM");
+    const bool sym = e ? atoi(e) != 0 : in.rows.nwin >= 450000;
+    if (!sym) return launch_join<8, true, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
+    return launch_join<8, true, false, true>(in, d_best_c, d_best_j, arena, st, err, launches);
+  }
+  return launch_join<8, false, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
 }
 
 int run_epilogue(const double* d_best_c, const int64_t* d_best_j, const uint8_t* d_row_flag, int64_t nrows,

@@ -124,8 +124,8 @@ int heads_fft_supported(int m);
 // ulp below it is a strict lower bound the join starts from (k_join).
 int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrows, const double* d_mua,
                       const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
-                      unsigned long long* d_seed, long long excl, Arena& arena, cudaStream_t st, int* launches,
-                      Error* err);
+                      unsigned long long* d_seed, long long excl, int sym, Arena& arena, cudaStream_t st,
+                      int* launches, Error* err);
 
 // Epilogue: corr -> distance (series.hpp:153-161), concat column -> source
 // coordinate (dictionary.hpp:183-188), (inf, -1) sentinel for rows without an

@@ -143,11 +143,15 @@ def test_self_join_exclusion_parameter_ecg(excl):
     check_profile(P.values, P.indices, rv, ri, m, ab_dist(t, t, m), label=f"self excl={excl}")
 
 
-def test_self_join_large_sampled_rows_virtual_segments():
-    """n = 2^18 self-join (one long segment cut into virtual column pieces,
-    several segment groups, exclusion-aware head seeds) and a 2^16 x 2^18
+@pytest.mark.parametrize("sym", ["1", "0"])
+def test_self_join_large_sampled_rows_virtual_segments(monkeypatch, sym):
+    """n = 2^18 self-join through the symmetric upper-triangle sweep (sym=1:
+    column side, 128-bit CAS candidates, dynamic task queue) and the
+    full-matrix sweep (sym=0; one long segment cut into virtual column pieces,
+    several segment groups, exclusion-aware head seeds), plus a 2^16 x 2^18
     AB-join: sampled rows against the oracle, each row's admissible set
     restated as a two-segment dictionary around its exclusion zone."""
+    monkeypatch.setenv("TSD_SYM", sym)
     n, m = 1 << 18, 256
     t = synth.walk(51, n)
     P = tsd.self_join(t, m)
@@ -170,6 +174,22 @@ def test_self_join_large_sampled_rows_virtual_segments():
         rv, ri = O.ab_join(a[i:i + m], t, m)
         check_profile(Q.values[i:i + 1], Q.indices[i:i + 1], rv, ri, m, ab_dist(a[i:i + m], t, m),
                       label=f"ab 2^16 x 2^18 row {i}")
+
+
+def test_symmetric_self_join_deterministic_and_equal_to_full(monkeypatch):
+    """the symmetric sweep (dynamic task order, atomics) is bit-identical
+    across runs, and matches the full-matrix sweep within the parity rule
+    (both evaluate every pair; only the diagonal start points differ)"""
+    t, _ = synth.ecg(12, 60000)
+    m = 250
+    monkeypatch.setenv("TSD_SYM", "1")
+    runs = [tsd.self_join(t, m, excl=62) for _ in range(3)]
+    for r in runs[1:]:
+        assert np.array_equal(r.values, runs[0].values) and np.array_equal(r.indices, runs[0].indices)
+    monkeypatch.setenv("TSD_SYM", "0")
+    full = tsd.self_join(t, m, excl=62)
+    check_profile(runs[0].values, runs[0].indices, full.values, full.indices, m, ab_dist(t, t, m),
+                  label="sym vs full")
 
 
 def test_flat_windows_ab_and_self():
