@@ -306,12 +306,43 @@ def run_gpu(args):
                     "d2h_bytes_per_step": int(nrows * 16), "api": "tsd_dict_join (host buffers, pinned)",
                     "matches_device_path": same},
             "gpu_launches": launches, "clocks": clk.summary(),
+            "self_join": self_join_lines(q, peak),
             "join_ms_median": jms, "fraction_of_fp64_peak_cells": (cells_per_step() / (jms * 1e-3)) /
                                                                     (peak / FLOPS_PER_CELL)}
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def self_join_lines(q, peak):
+    """Self-join throughput in the reference's unit (one admissible unordered
+    pair |i - j| > excl evaluated once, profiles.hpp:287-297):
+    the SURVEY's proposed target (a 2^21 prefix of the C4 query, m = 512,
+    excl = m/2) and BASELINE C2 (ECG-like, n = 131072, m = 250, excl = m/4).
+    Host API (tsd_self_join), so host<->device copies are inside the time."""
+    import torch
+    import paper_2112_12965_b200 as tsd
+    from paper_2112_12965_b200 import synth
+    out = {}
+    for name, x, m, excl in (("self_2^21_m512", np.ascontiguousarray(q[: 1 << 21]), 512, None),
+                             ("C2_self_ecg_m250", synth.ecg(2, 131072)[0], 250, 62)):
+        cnt = x.size - m + 1
+        e = m // 2 if excl is None else excl
+        pairs = (cnt - e - 1) * (cnt - e) / 2
+        tsd.self_join(x, m, excl=excl)  # warm
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tsd.self_join(x, m, excl=excl)
+            ts.append(time.perf_counter() - t0)
+        t = statistics.median(ts)
+        out[name] = {"n": int(x.size), "m": m, "excl": e, "pairs": pairs, "ms": t * 1e3,
+                     "value": pairs / t / 1e9, "unit": "GPair/s",
+                     "frac_of_fp64_cell_peak": pairs / t / (peak / FLOPS_PER_CELL),
+                     "kernel": "symmetric upper-triangle sweep" if cnt >= 450000 else "full-matrix sweep"}
+    return out
 
 
 def committed_traffic():
