@@ -110,6 +110,30 @@ int tsd_dict_plan_last_timing(tsd_dict_plan* plan, double* step_ms, double* join
  * heads were computed inside the join kernel). */
 int tsd_dict_plan_last_kernel_timing(tsd_dict_plan* plan, double* join_kernel_ms, double* heads_ms);
 
+/* ---- greedy dictionary learning (dictionary.hpp:259-328) ----
+ * learn_dictionary on the device: argmin of the processed profile P - S over
+ * unmasked windows, masking, context intervals and merging as the reference's
+ * select_state, distance profiles of the picks (exact FP64 dot products: the
+ * 1 x n slice of the join, MASS's rules without its FFT round-off), stop
+ * rules, then compute_e_max of the result. Exactly one stop rule: rule =
+ * TSD_RULE_SPACE_SAVING (rule_value = target fraction in [0, 1)),
+ * TSD_RULE_SAMPLE_BUDGET (samples > 0) or TSD_RULE_ERROR_TARGET (e_max
+ * target >= 0). profile: the exact self-join profile values of t (n-m+1
+ * doubles, as learn_dictionary(T, cfg, P_B)) or NULL to compute it here
+ * (self_join with excl = m/2). Outputs (caller-allocated): merged segments
+ * (seg_start, seg_len: capacity n; seg_vals: capacity n samples), their count
+ * *nseg, core starts in pick order (capacity n-m+1) and *ncores, e_max,
+ * space_saving, no_progress. Validation order as validate_learn_config
+ * (:120-141), then series_too_short (n < 2m); iteration_cap_exceeded when
+ * max_iterations picks pass without the stop rule firing. */
+#define TSD_RULE_SPACE_SAVING 0
+#define TSD_RULE_SAMPLE_BUDGET 1
+#define TSD_RULE_ERROR_TARGET 2
+int tsd_learn_dictionary(const double* t, size_t n, size_t m, double k, int rule, double rule_value,
+                         size_t max_iterations, const double* profile, size_t* seg_start, size_t* seg_len,
+                         double* seg_vals, size_t* nseg, size_t* core_starts, size_t* ncores, double* e_max,
+                         double* space_saving, int* no_progress);
+
 /* ---- diagnostics ---- */
 const char* tsd_last_error(void);
 const char* tsd_status_name(int status); /* reference errc_name (errors.hpp:37-57) */

@@ -132,6 +132,87 @@ def pair_dist(a, i, b, j, m):
     return lib().tsdo_pair_dist(_p(a, _f64p), a.size, i, _p(b, _f64p), b.size, j, m)
 
 
+def _kahan_mean_sd(q):
+    """MASS's query statistics: Kahan mean, Kahan two-pass std (profiles.hpp:203-213)"""
+    s = c = 0.0
+    for x in q:
+        y = x - c
+        t = s + y
+        c = (t - s) - y
+        s = t
+    mu = s / q.size
+    s = c = 0.0
+    for x in q:
+        y = (x - mu) * (x - mu) - c
+        t = s + y
+        c = (t - s) - y
+        s = t
+    return mu, np.sqrt(max(0.0, s / q.size))
+
+
+def learn_dictionary_replay(t, m, k=1.5, rule=0, value=0.5, max_iterations=1000000):
+    """ORACLE restatement of the greedy learning loop (dictionary.hpp:259-321,
+    replayed the way test_dictionary.cpp:94-158 does): argmin of P - S over
+    unmasked windows (first minimum), select_state masking / context
+    intervals / merging, distance profiles of the picks folded into S, stop
+    rules. P is this oracle's self_join (bit-identical to the reference);
+    distance profiles are exact dot products (MASS without its FFT round-off,
+    with its constant-window rules). Returns (cores, merged intervals,
+    no_progress)."""
+    t = _f(t)
+    n, cnt, excl = t.size, t.size - m + 1, m // 2
+    P, _ = self_join(t, m)
+    mu, _, invn, flat = compute_stats(t, m)
+    W = np.lib.stride_tricks.sliding_window_view(t, m) - mu[:, None]
+    far = np.sqrt(2.0 * m)
+    total = int(k * m + 1e-9)
+    before = total // 2
+    masked = np.zeros(cnt, dtype=bool)
+    S = np.zeros(cnt)
+    s_init, cores, ivs, stall = False, [], [], False
+    need = value if rule == 1 else (1.0 - value) * n - 1e-6
+    for it in range(max_iterations + 1):
+        if it >= max_iterations:
+            raise RuntimeError("iteration cap")
+        cand = np.where(~masked)[0]
+        if cand.size == 0:
+            stall = True
+            break
+        j = int(cand[np.argmin(P[cand] - S[cand])])  # argmin returns the first minimum
+        cores.append(j)
+        masked[max(0, j - excl): min(cnt, j + excl + 1)] = True
+        ivs.append((max(0, j - before), min(n, j + m + (total - before))))
+        merged = []
+        for lo, hi in sorted(ivs):
+            if merged and lo <= merged[-1][1]:
+                merged[-1] = (merged[-1][0], max(merged[-1][1], hi))
+            else:
+                merged.append((lo, hi))
+        if rule != 2 and sum(hi - lo for lo, hi in merged) >= need:
+            break
+        q = t[j:j + m]
+        mq, sq = _kahan_mean_sd(q)
+        if sq < 1e-8 * max(1.0, float(np.max(np.abs(q)))):
+            dp = np.where(flat & 2 > 0, 0.0, far)
+        else:
+            rho = (W @ (q - mq)) * invn / (sq * np.sqrt(m))
+            dp = np.sqrt(np.clip(2.0 * m * (1.0 - np.clip(rho, -1.0, 1.0)), 0.0, 4.0 * m))
+            dp[flat & 2 > 0] = far
+            if not flat[j] & 2:
+                dp[j] = pair_dist(t, j, t, j, m)
+        S = dp if not s_init else np.minimum(S, dp)
+        s_init = True
+        if rule == 2 and S.max() <= value:
+            break
+    merged = []
+    for lo, hi in sorted(ivs):
+        if merged and lo <= merged[-1][1]:
+            merged[-1] = (merged[-1][0], max(merged[-1][1], hi))
+        else:
+            merged.append((lo, hi))
+    return cores, merged, stall
+
+
 def ab_join_brute(a, b, m):
     a, b = _f(a), _f(b)
     cnt = a.size - m + 1
@@ -214,6 +295,31 @@ def ref_sine(n, period, amp=1.0):
     o = np.empty(n)
     ref().tsdr_sine(n, period, amp, _p(o, _f64p))
     return o
+
+
+def ref_learn_dictionary_full(t, m, k=1.5, rule=0, value=0.5, max_iterations=1000000, threads=0):
+    """the reference's learn_dictionary with any stop rule (0 space saving,
+    1 sample budget, 2 error target); returns a dict with starts, lengths,
+    cores, e_max, space_saving, no_progress"""
+    t = _f(t)
+    n = t.size
+    st = np.zeros(n, dtype=np.uintp)
+    ln = np.zeros(n, dtype=np.uintp)
+    vals = np.zeros(n)
+    cores = np.zeros(n, dtype=np.uintp)
+    ns, nc = ctypes.c_size_t(), ctypes.c_size_t()
+    em, ss, npg = ctypes.c_double(), ctypes.c_double(), ctypes.c_int()
+    r = ref()
+    r.tsdr_learn_dictionary2.argtypes = [_f64p, _sz, _sz, ctypes.c_double, ctypes.c_int, ctypes.c_double, _sz,
+                                         ctypes.c_uint, _szp, _szp, _f64p, ctypes.POINTER(ctypes.c_size_t), _szp,
+                                         ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_double),
+                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int)]
+    _chk(r.tsdr_learn_dictionary2(_p(t, _f64p), n, m, k, rule, value, max_iterations, threads, _p(st, _szp),
+                                  _p(ln, _szp), _p(vals, _f64p), ctypes.byref(ns), _p(cores, _szp), ctypes.byref(nc),
+                                  ctypes.byref(em), ctypes.byref(ss), ctypes.byref(npg)))
+    return {"starts": st[:ns.value].astype(np.int64), "lengths": ln[:ns.value].astype(np.int64),
+            "cores": cores[:nc.value].astype(np.int64), "e_max": em.value, "space_saving": ss.value,
+            "no_progress": int(npg.value)}
 
 
 def ref_learn_dictionary(t, m, space_saving, threads=0):

@@ -127,6 +127,37 @@ int tsdr_learn_dictionary(const double* t, size_t n, size_t m, double space_savi
   });
 }
 
+// learn_dictionary with any stop rule (rule 0: space saving, 1: sample budget,
+// 2: error target); also returns the core starts, space_saving, no_progress
+int tsdr_learn_dictionary2(const double* t, size_t n, size_t m, double k, int rule, double value,
+                           size_t max_iterations, unsigned threads, size_t* seg_start, size_t* seg_len,
+                           double* seg_vals, size_t* nseg, size_t* cores, size_t* ncores, double* e_max,
+                           double* space_saving, int* no_progress) {
+  return guarded([&] {
+    tsdict::LearnConfig cfg;
+    cfg.m = m;
+    cfg.k = k;
+    if (rule == 0) cfg.space_saving_target = value;
+    if (rule == 1) cfg.sample_budget = (size_t)value;
+    if (rule == 2) cfg.error_target = value;
+    cfg.max_iterations = max_iterations;
+    const tsdict::Dictionary D = tsdict::learn_dictionary(ts(t, n), cfg, threads);
+    size_t off = 0;
+    for (size_t s = 0; s < D.segments.size(); ++s) {
+      seg_start[s] = D.segments[s].start;
+      seg_len[s] = D.segments[s].length();
+      std::memcpy(seg_vals + off, D.segments[s].values.data(), seg_len[s] * sizeof(double));
+      off += seg_len[s];
+    }
+    *nseg = D.segments.size();
+    for (size_t c = 0; c < D.core_starts.size(); ++c) cores[c] = D.core_starts[c];
+    *ncores = D.core_starts.size();
+    *e_max = D.e_max.value_or(-1.0);
+    *space_saving = D.space_saving;
+    *no_progress = D.no_progress ? 1 : 0;
+  });
+}
+
 // tests/oracles.hpp long-double brute force
 int tsdr_ab_join_brute(const double* a, size_t na, const double* b, size_t nb, size_t m, double* val,
                        int64_t* idx) {

@@ -28,6 +28,8 @@ __all__ = [
     "compute_stats", "ab_join", "self_join", "join_dictionary", "dict_min_profile", "compute_e_max",
     "join_dictionary_batched", "corr_to_dist", "DictPlan", "load_library", "measure_peak", "build_info",
     "C_SYMBOLS",
+    "LearnConfig",
+    "learn_dictionary",
 ]
 
 
@@ -95,6 +97,8 @@ C_SYMBOLS = {
     "tsd_dict_join": (_int, [_f64p, _sz, _f64p, _szp, _szp, _sz, _sz, _int, _f64p, _i64p]),
     "tsd_dict_join_batched": (_int, [_f64p, _szp, _sz, _f64p, _szp, _szp, _sz, _sz, _int, _f64p, _i64p]),
     "tsd_compute_e_max": (_int, [_f64p, _sz, _sz, _f64p, _szp, _szp, _sz, _sz, _f64p]),
+    "tsd_learn_dictionary": (_int, [_f64p, _sz, _sz, ctypes.c_double, _int, ctypes.c_double, _sz, _f64p, _szp, _szp,
+                                    _f64p, _szp, _szp, _szp, _f64p, _f64p, ctypes.POINTER(_int)]),
     "tsd_dict_plan_create": (_int, [_f64p, _szp, _szp, _sz, _sz, _int, ctypes.POINTER(_vp)]),
     "tsd_dict_plan_join_device": (_int, [_vp, _vp, _szp, _sz, _vp, _vp, _vp]),
     "tsd_dict_plan_join": (_int, [_vp, _f64p, _szp, _sz, _f64p, _i64p]),
@@ -310,6 +314,57 @@ def compute_e_max(D: Dictionary, T_B, threads: int = 0) -> float:
     _check(lib.tsd_compute_e_max(_ptr(x, _f64p), x.size, D.source_length, _ptr(vals, _f64p), _ptr(lens, _szp),
                                  _ptr(starts, _szp), len(D.segments), D.m, ctypes.byref(out)))
     return out.value
+
+
+@dataclass
+class LearnConfig:
+    """dictionary.hpp:57-64 (exactly one stop rule)."""
+    m: int = 0
+    k: float = 1.5
+    space_saving_target: Optional[float] = None
+    sample_budget: Optional[int] = None
+    error_target: Optional[float] = None
+    max_iterations: int = 1000000
+
+
+def learn_dictionary(T_B, cfg: LearnConfig, P_B: Optional[MatrixProfile] = None, threads: int = 0) -> Dictionary:
+    """dictionary.hpp:259-328: greedy selection on the device, then compute_e_max.
+    P_B: the exact self-join profile of T_B (learn_dictionary(T_B, cfg, P_B))."""
+    x = _vals(T_B)
+    n, m = x.size, cfg.m
+    rules = [r for r in (cfg.space_saving_target, cfg.sample_budget, cfg.error_target) if r is not None]
+    if len(rules) != 1:
+        raise TsdictError(errc.invalid_argument, "exactly one stop rule must be set")
+    if cfg.space_saving_target is not None:
+        rule, val = 0, float(cfg.space_saving_target)
+    elif cfg.sample_budget is not None:
+        rule, val = 1, float(cfg.sample_budget)
+    else:
+        rule, val = 2, float(cfg.error_target)
+    prof = None
+    if P_B is not None:  # :267-271
+        if n >= 2 * m and (P_B.m != m or P_B.kind != "self" or P_B.values.size != n - m + 1):
+            raise TsdictError(errc.invalid_argument, "precomputed profile does not match the series and window")
+        prof = _f64(P_B.values)
+    cap = max(n, 1)
+    starts = np.zeros(cap, dtype=np.uintp)
+    lens = np.zeros(cap, dtype=np.uintp)
+    vals = np.zeros(cap)
+    cores = np.zeros(cap, dtype=np.uintp)
+    nseg, ncores = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    e, ss, npg = ctypes.c_double(0.0), ctypes.c_double(0.0), ctypes.c_int(0)
+    lib = load_library()
+    _check(lib.tsd_learn_dictionary(_ptr(x, _f64p), n, m, cfg.k, rule, val, cfg.max_iterations,
+                                    _ptr(prof, _f64p) if prof is not None else None, _ptr(starts, _szp),
+                                    _ptr(lens, _szp), _ptr(vals, _f64p), ctypes.byref(nseg), _ptr(cores, _szp),
+                                    ctypes.byref(ncores), ctypes.byref(e), ctypes.byref(ss), ctypes.byref(npg)))
+    segs, off = [], 0
+    for s in range(nseg.value):
+        L = int(lens[s])
+        segs.append(Segment(int(starts[s]), vals[off:off + L].copy()))
+        off += L
+    return Dictionary(segments=segs, m=m, k=cfg.k, source_length=n, core_starts=[int(c) for c in cores[:ncores.value]],
+                      e_max=e.value, space_saving=ss.value, no_progress=bool(npg.value))
 
 
 class DictPlan:

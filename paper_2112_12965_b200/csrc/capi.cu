@@ -295,7 +295,7 @@ int tsd_compute_stats(const double* x, size_t n, size_t m, double* means, double
 
 // shared by ab_join and self_join: one series of rows, one segment of columns
 static int single_join(const double* a, size_t na, const double* b, size_t nb, size_t m, int64_t excl, int precision,
-                       double* val, int64_t* idx) {
+                       double* val, int64_t* idx, bool force_sym = false) {
   ThreadCtx& tc = tctx();
   if (int rc = tc.s.init()) return rc;
   tc.arena.reset();
@@ -309,6 +309,7 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
   if (!self) CK(cudaMemcpyAsync(d_b, b, sizeof(double) * nb, cudaMemcpyHostToDevice, st));
   Error er{0, ""};
   JoinInputs in;
+  in.force_sym = force_sym;
   std::vector<Group> ga;
   add_groups(ga, 0, (int64_t)na, (int)m, 0, 0);
   int bad = -1;
@@ -428,6 +429,197 @@ int tsd_dict_plan_join(tsd_dict_plan* plan, const double* q, const size_t* q_len
                        int64_t* idx) {
   if (!plan) return fail(kInvalidArgument, "null plan");
   return plan_join_host(plan, q, q_len, nseries, val, idx);
+}
+
+// ---------------------------------------------------------------------------
+// greedy dictionary learning (dictionary.hpp:259-328)
+// ---------------------------------------------------------------------------
+namespace {
+struct Kahan {  // series.hpp:49-60
+  double sum = 0.0, comp = 0.0;
+  void add(double x) {
+    const double y = x - comp;
+    const double t = sum + y;
+    comp = (t - sum) - y;
+    sum = t;
+  }
+};
+double constancy_threshold_h(double max_abs) { return 1e-8 * std::max(1.0, max_abs); }  // series.hpp:75-77
+double corr_to_dist_h(double rho, size_t m) {                                            // series.hpp:153-161
+  if (rho > 1.0) rho = 1.0;
+  if (rho < -1.0) rho = -1.0;
+  double d = std::sqrt(2.0 * (double)m * (1.0 - rho));
+  const double dmax = 2.0 * std::sqrt((double)m);
+  if (d < 0.0) d = 0.0;
+  if (d > dmax) d = dmax;
+  return d;
+}
+// znorm_distance (series.hpp:166-203): the exact origin entry of MASS
+double znorm_distance_h(const double* a, const double* b, size_t m) {
+  double max_abs = 0.0;
+  Kahan sa, sb;
+  for (size_t i = 0; i < m; ++i) {
+    sa.add(a[i]);
+    sb.add(b[i]);
+    max_abs = std::max({max_abs, std::fabs(a[i]), std::fabs(b[i])});
+  }
+  const double md = (double)m, mu_a = sa.sum / md, mu_b = sb.sum / md;
+  Kahan va, vb, cov;
+  for (size_t i = 0; i < m; ++i) {
+    const double da = a[i] - mu_a, db = b[i] - mu_b;
+    va.add(da * da);
+    vb.add(db * db);
+    cov.add(da * db);
+  }
+  const double sd_a = std::sqrt(std::max(0.0, va.sum / md)), sd_b = std::sqrt(std::max(0.0, vb.sum / md));
+  const double eps = constancy_threshold_h(max_abs);
+  const bool fa = sd_a < eps, fb = sd_b < eps;
+  if (fa && fb) return 0.0;
+  if (fa || fb) return std::sqrt(2.0 * md);
+  return corr_to_dist_h(cov.sum / (md * (sd_a * sd_b)), m);
+}
+typedef std::pair<size_t, size_t> Interval;
+Interval context_interval_h(size_t j, size_t m, double k, size_t n) {  // dictionary.hpp:78-84
+  const size_t total = (size_t)(k * (double)m + 1e-9);
+  const size_t before = total / 2;
+  return {j >= before ? j - before : 0, std::min(n, j + m + (total - before))};
+}
+std::vector<Interval> merge_intervals_h(std::vector<Interval> iv) {  // :87-98
+  std::sort(iv.begin(), iv.end());
+  std::vector<Interval> out;
+  for (const auto& x : iv) {
+    if (!out.empty() && x.first <= out.back().second)
+      out.back().second = std::max(out.back().second, x.second);
+    else
+      out.push_back(x);
+  }
+  return out;
+}
+}  // namespace
+
+int tsd_learn_dictionary(const double* t, size_t n, size_t m, double k, int rule, double rule_value,
+                         size_t max_iterations, const double* profile, size_t* seg_start, size_t* seg_len,
+                         double* seg_vals, size_t* nseg, size_t* core_starts, size_t* ncores, double* e_max,
+                         double* space_saving, int* no_progress) {
+  // validate_learn_config (dictionary.hpp:120-141), then :267
+  if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");
+  if (!(k >= 0.0)) return fail(kInvalidArgument, "context factor k must be non-negative");
+  if (rule != TSD_RULE_SPACE_SAVING && rule != TSD_RULE_SAMPLE_BUDGET && rule != TSD_RULE_ERROR_TARGET)
+    return fail(kInvalidArgument, "exactly one stop rule must be set");
+  if (rule == TSD_RULE_SPACE_SAVING && (rule_value < 0.0 || rule_value >= 1.0))
+    return fail(kInvalidArgument, "space saving target must lie in [0, 1)");
+  if (rule == TSD_RULE_SAMPLE_BUDGET && !(rule_value >= 1.0))
+    return fail(kInvalidArgument, "sample budget must be positive");
+  if (rule == TSD_RULE_ERROR_TARGET && rule_value < 0.0)
+    return fail(kInvalidArgument, "error target must be non-negative");
+  if (max_iterations == 0) return fail(kInvalidArgument, "iteration cap must be positive");
+  if (n < 2 * m) return fail(kSeriesTooShort, "dictionary learning needs n >= 2m");
+  const size_t cnt = n - m + 1, excl = m / 2;
+  // the exact self-join profile P_B (dictionary.hpp:325-327)
+  std::vector<double> P(cnt);
+  if (profile) {
+    std::copy(profile, profile + cnt, P.begin());
+  } else {
+    // symmetric sweep: a pair's two rows carry the bitwise-identical value, so
+    // argmin ties (mutual nearest neighbours) resolve as the reference's do
+    std::vector<int64_t> ix(cnt);
+    if (int rc = single_join(t, n, nullptr, 0, m, (int64_t)(m / 2), TSD_FP64, P.data(), ix.data(), true)) return rc;
+  }
+  ThreadCtx& tc = tctx();
+  if (int rc = tc.s.init()) return rc;
+  cudaStream_t st = tc.s.st;
+  Arena ar;  // the loop's own buffers (tsd_* calls below reset the thread arena)
+  double* d_x = (double*)ar.get(sizeof(double) * (n + 64));
+  double* d_P = (double*)ar.get(sizeof(double) * cnt);
+  double* d_S = (double*)ar.get(sizeof(double) * cnt);
+  double* d_qc = (double*)ar.get(sizeof(double) * m);
+  uint8_t* d_mask = (uint8_t*)ar.get(cnt);
+  void* d_scr = ar.get(learn_scratch_bytes());
+  if (!d_x || !d_P || !d_S || !d_qc || !d_mask || !d_scr) return fail(kCudaError, "device allocation failed");
+  CK(cudaMemcpyAsync(d_x, t, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_P, P.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(d_S, 0, sizeof(double) * cnt, st));
+  CK(cudaMemsetAsync(d_mask, 0, cnt, st));
+  std::vector<Group> g;
+  add_groups(g, 0, (int64_t)n, (int)m, 0, 0);
+  WindowArrays w;
+  Error er{0, ""};
+  int bad = -1;
+  TRY(compute_windows(d_x, (int64_t)n, (int)m, g, 1, w, ar, st, &bad, &er));
+  if (bad >= 0) return fail(kNonFiniteInput, "series contains a non-finite sample");
+  std::vector<uint8_t> hflag(cnt);
+  CK(cudaMemcpyAsync(hflag.data(), w.flag, cnt, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+
+  const bool budget_rule = rule != TSD_RULE_ERROR_TARGET;
+  const double need = rule == TSD_RULE_SAMPLE_BUDGET ? rule_value : (1.0 - rule_value) * (double)n - 1e-6;  // :244-247
+  std::vector<Interval> chosen, merged;
+  std::vector<size_t> cores;
+  size_t stored = 0;
+  bool s_init = false, stall = false;
+  std::vector<double> qc(m);
+  for (size_t iter = 0;; ++iter) {
+    if (iter >= max_iterations)
+      return fail(kIterationCapExceeded, "iteration cap reached before the stop rule fired");
+    double bv = 0.0;
+    int64_t j = -1;
+    if (learn_argmin(d_P, d_S, d_mask, (int64_t)cnt, d_scr, &bv, &j, st) != kOk)
+      return fail(kCudaError, std::string("learning argmin: ") + cudaGetErrorString(cudaGetLastError()));
+    if (j < 0) {
+      stall = true;
+      break;
+    }
+    // select_state::take (dictionary.hpp:213-224)
+    cores.push_back((size_t)j);
+    chosen.push_back(context_interval_h((size_t)j, m, k, n));
+    merged = merge_intervals_h(chosen);
+    stored = 0;
+    for (const auto& iv : merged) stored += iv.second - iv.first;
+    const size_t lo = (size_t)j >= excl ? (size_t)j - excl : 0, hi = std::min(cnt, (size_t)j + excl + 1);
+    CK(cudaMemsetAsync(d_mask + lo, 1, hi - lo, st));
+    if (budget_rule && (double)stored >= need) break;
+    // distance profile of window j (profiles.hpp:186-260) folded into S
+    const double* Q = t + j;
+    double max_abs = 0.0;
+    Kahan qs;
+    for (size_t i = 0; i < m; ++i) {
+      qs.add(Q[i]);
+      max_abs = std::max(max_abs, std::fabs(Q[i]));
+    }
+    const double md = (double)m, mu_q = qs.sum / md;
+    Kahan qv;
+    for (size_t i = 0; i < m; ++i) qv.add((Q[i] - mu_q) * (Q[i] - mu_q));
+    const double sd_q = std::sqrt(std::max(0.0, qv.sum / md));
+    const bool cq = sd_q < constancy_threshold_h(max_abs);
+    const double invn_q = cq ? 0.0 : 1.0 / (sd_q * std::sqrt(md));
+    for (size_t i = 0; i < m; ++i) qc[i] = Q[i] - mu_q;
+    const double origin = (hflag[j] & 2) ? 0.0 : znorm_distance_h(Q, t + j, m);
+    CK(cudaMemcpyAsync(d_qc, qc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, st));
+    if (learn_dprof_fold(d_x, w, (int)m, d_qc, invn_q, cq, j, origin, !s_init, d_S, st) != kOk)
+      return fail(kCudaError, std::string("distance profile: ") + cudaGetErrorString(cudaGetLastError()));
+    s_init = true;
+    if (rule == TSD_RULE_ERROR_TARGET) {  // :305-309
+      double worst = 0.0;
+      if (learn_max(d_S, (int64_t)cnt, d_scr, &worst, st) != kOk)
+        return fail(kCudaError, std::string("learning max: ") + cudaGetErrorString(cudaGetLastError()));
+      if (worst <= rule_value) break;
+    }
+  }
+  // finish_dictionary (dictionary.hpp:226-237)
+  size_t off = 0;
+  for (size_t s = 0; s < merged.size(); ++s) {
+    seg_start[s] = merged[s].first;
+    seg_len[s] = merged[s].second - merged[s].first;
+    std::copy(t + merged[s].first, t + merged[s].second, seg_vals + off);
+    off += seg_len[s];
+  }
+  *nseg = merged.size();
+  for (size_t c = 0; c < cores.size(); ++c) core_starts[c] = cores[c];
+  *ncores = cores.size();
+  *space_saving = 1.0 - (double)stored / (double)n;
+  *no_progress = stall ? 1 : 0;
+  // D.e_max = compute_e_max(D, T_B) (:319)
+  return tsd_compute_e_max(t, n, n, seg_vals, seg_len, seg_start, merged.size(), m, e_max);
 }
 
 int tsd_dict_plan_destroy(tsd_dict_plan* plan) {

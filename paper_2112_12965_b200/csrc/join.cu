@@ -354,7 +354,10 @@ __device__ __noinline__ void col_update(const double* vals, const double* __rest
       const long long d = col - row;
       const double ia = row < nrows ? invn_a[row] : 0.0;
       if ((d > excl || d < -excl) && ia > 0.0) {
-        const double c = clamp_corr(vals[r * 32 + lane] * ia * invb);  // profiles.hpp:289-294
+        // the same rounding as the row side's clamp((cov * invn_b) * invn_a):
+        // both rows of a pair see the bitwise-identical correlation, as in the
+        // reference (one value updates both, profiles.hpp:289-296)
+        const double c = clamp_corr(vals[r * 32 + lane] * invb * ia);
         const unsigned long long k = order_key(c);
         if (k > bk || (k == bk && (unsigned)row < brow)) {
           bk = k;
@@ -1735,7 +1738,7 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     // that the full-matrix sweep (every pair from both rows) is faster.
     // TSD_SYM=1 / 0 forces either.
     const char* e = getenv("TSD_SYM");
-    const bool sym = e ? atoi(e) != 0 : in.rows.nwin >= 450000;
+    const bool sym = in.force_sym || (e ? atoi(e) != 0 : in.rows.nwin >= 450000);
     if (!sym) return launch_join<8, true, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
     return launch_join<8, true, false, true>(in, d_best_c, d_best_j, arena, st, err, launches);
   }

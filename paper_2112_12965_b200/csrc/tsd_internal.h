@@ -102,6 +102,7 @@ struct JoinInputs {
   int m;
   int64_t excl = -1;  // self-join exclusion half-width (|i-j| <= excl rejected); -1 = AB join
   int precision;      // 0 fp64, 1 fp32
+  bool force_sym = false;  // self-join: the symmetric sweep at any size (bitwise-equal pair values)
   // optional timing events: [0, 1] around the FFT heads pre-pass, [2, 3]
   // around the join kernel (recorded when non-null); heads_used set by run_join
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -126,6 +127,17 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
                       const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
                       unsigned long long* d_seed, long long excl, int sym, Arena& arena, cudaStream_t st,
                       int* launches, Error* err);
+
+// learn.cu -------------------------------------------------------------------
+// Device steps of the greedy learning loop (dictionary.hpp:279-316): argmin of
+// P - S over unmasked windows (lexicographic, first minimum), max of S, and the
+// exact FP64 distance profile of a picked window folded into S.
+int learn_argmin(const double* d_P, const double* d_S, const uint8_t* d_mask, int64_t cnt, void* d_scratch,
+                 double* h_val, int64_t* h_idx, cudaStream_t st);
+int learn_max(const double* d_S, int64_t cnt, void* d_scratch, double* h_max, cudaStream_t st);
+int learn_dprof_fold(const double* d_x, const WindowArrays& w, int m, const double* d_qc, double invn_q,
+                     bool const_query, int64_t origin, double origin_val, bool first, double* d_S, cudaStream_t st);
+size_t learn_scratch_bytes();
 
 // Epilogue: corr -> distance (series.hpp:153-161), concat column -> source
 // coordinate (dictionary.hpp:183-188), (inf, -1) sentinel for rows without an

@@ -185,6 +185,80 @@ int main() {
     const double e = compute_e_max(D, T);
     return e <= 1e-5 ? "" : "e_max " + std::to_string(e);
   });
+  // learn_dictionary (test_dictionary.cpp:53-82 invariants, :250-400 rules)
+  auto invariants = [](const Dictionary& D, const TimeSeries& T) -> std::string {
+    if (D.source_length != T.n() || D.segments.empty()) return "empty or wrong source length";
+    std::size_t stored = 0, prev_end = 0;
+    for (std::size_t s = 0; s < D.segments.size(); ++s) {
+      const auto& g = D.segments[s];
+      if (g.length() < D.m || g.start + g.length() > T.n()) return "segment bounds";
+      if (s > 0 && g.start <= prev_end) return "segments not disjoint / sorted / separated";
+      prev_end = g.start + g.length();
+      for (std::size_t i = 0; i < g.length(); ++i)
+        if (g.values[i] != T.values[g.start + i]) return "segment is not a verbatim copy";
+      stored += g.length();
+    }
+    if (std::fabs(D.space_saving - (1.0 - double(stored) / double(T.n()))) > 1e-12) return "space_saving";
+    for (std::size_t a = 0; a < D.core_starts.size(); ++a)
+      for (std::size_t b = a + 1; b < D.core_starts.size(); ++b) {
+        const std::size_t lo = std::min(D.core_starts[a], D.core_starts[b]);
+        const std::size_t hi = std::max(D.core_starts[a], D.core_starts[b]);
+        if (hi - lo <= D.m / 2) return "core starts closer than the exclusion zone";
+      }
+    return "";
+  };
+  check("LearnDictionary.InvariantsAndBudget", [&] {
+    Rng r(90);
+    const TimeSeries T{r.walk(3000)};
+    LearnConfig cfg;
+    cfg.m = 50;
+    cfg.space_saving_target = 0.5;
+    const Dictionary D = learn_dictionary(T, cfg);
+    if (auto e = invariants(D, T); !e.empty()) return e;
+    if (double(D.stored_samples()) < 0.5 * 3000 - 1e-6) return std::string("budget rule did not hold");
+    if (!D.e_max || *D.e_max <= 0.0) return std::string("e_max not set");
+    return std::string();
+  });
+  check("LearnDictionary.PrecomputedProfileOverload", [&] {
+    Rng r(91);
+    const TimeSeries T{r.walk(2000)};
+    LearnConfig cfg;
+    cfg.m = 60;
+    cfg.sample_budget = 600;
+    const Dictionary a = learn_dictionary(T, cfg);
+    const Dictionary b = learn_dictionary(T, cfg, self_join(T, 60));
+    return a.core_starts == b.core_starts && *a.e_max == *b.e_max ? std::string() : std::string("overloads differ");
+  });
+  check("LearnDictionaryRandom.DeterministicPerSeed", [&] {
+    Rng r(92);
+    const TimeSeries T{r.walk(2500)};
+    LearnConfig cfg;
+    cfg.m = 50;
+    cfg.space_saving_target = 0.7;
+    const Dictionary a = learn_dictionary_random(T, cfg, 42), b = learn_dictionary_random(T, cfg, 42);
+    const Dictionary c = learn_dictionary_random(T, cfg, 43);
+    if (auto e = invariants(a, T); !e.empty()) return e;
+    if (a.core_starts != b.core_starts) return std::string("same seed, different picks");
+    if (a.core_starts == c.core_starts) return std::string("different seeds, same picks");
+    return std::string();
+  });
+  check("LearnDictionary.Errors", [&] {
+    Rng r(93);
+    const TimeSeries T{r.walk(500)};
+    LearnConfig cfg;
+    cfg.m = 50;
+    if (auto e = expect_code(errc::invalid_argument, [&] { learn_dictionary(T, cfg); }); !e.empty()) return e;
+    cfg.space_saving_target = 0.5;
+    cfg.error_target = 1.0;
+    if (auto e = expect_code(errc::invalid_argument, [&] { learn_dictionary(T, cfg); }); !e.empty()) return e;
+    cfg.error_target.reset();
+    cfg.m = 300;
+    if (auto e = expect_code(errc::series_too_short, [&] { learn_dictionary(T, cfg); }); !e.empty()) return e;
+    cfg.m = 50;
+    cfg.error_target = 1.0;
+    cfg.space_saving_target.reset();
+    return expect_code(errc::invalid_argument, [&] { learn_dictionary_random(T, cfg, 1); });
+  });
   std::printf("%d failure(s)\n", failures);
   return failures;
 }

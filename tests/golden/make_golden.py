@@ -53,6 +53,14 @@ def main():
         d[f"{name}__val"], d[f"{name}__idx"] = v, i
         cases.append(("dict", name))
 
+    def learn_case(name, t, m, k, rule, value, max_iterations=1000000):
+        r = O.ref_learn_dictionary_full(t, m, k, rule, value, max_iterations, threads=3)
+        d[f"{name}__t"], d[f"{name}__m"], d[f"{name}__k"] = t, np.int64(m), np.float64(k)
+        d[f"{name}__rule"], d[f"{name}__value"] = np.int64(rule), np.float64(value)
+        for key, v in r.items():
+            d[f"{name}__{key}"] = np.asarray(v)
+        cases.append(("learn", name))
+
     # stats (test_series.cpp:42-69, :94-105)
     r = O.RefRng(101)
     stats_case("stats_noise2048_m64", r.noise(2048), 64)
@@ -114,6 +122,17 @@ def main():
     rs = O.RefRng(1)
     segs = [rs.walk(512) for _ in range(8)]
     dict_case("dict_C1", q, segs, [512 * s for s in range(8)], 100)
+    # greedy learning, every stop rule (test_dictionary.cpp:250-400 shapes):
+    # space saving, sample budget, error target, k = 0, no progress
+    learn_case("learn_saving_walk_80", O.RefRng(80).walk(3000), 50, 1.5, 0, 0.5)
+    learn_case("learn_budget_walk_81", O.RefRng(81).walk(2500), 60, 1.5, 1, 700)
+    learn_case("learn_error_walk_82", O.RefRng(82).walk(2000), 60, 1.5, 2, 3.0)
+    r = O.RefRng(83)
+    per = np.sin(2 * np.pi * np.arange(4000) / 97.0) + 0.05 * r.noise(4000)
+    learn_case("learn_saving_periodic_83", per, 100, 1.5, 0, 0.7)
+    learn_case("learn_k0_budget_walk_84", O.RefRng(84).walk(1800), 40, 0.0, 1, 400)
+    learn_case("learn_no_progress_85", O.RefRng(85).walk(1500), 100, 1.5, 1, 100000)
+    learn_case("learn_zero_saving_86", O.RefRng(86).walk(900), 60, 1.5, 0, 0.0)
     d["__cases__"] = np.asarray([f"{k}:{n}" for k, n in cases])
     np.savez_compressed(OUT, **d)
     print(f"wrote {OUT}: {len(cases)} cases, {os.path.getsize(OUT) / 1024:.0f} KiB")

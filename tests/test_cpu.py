@@ -152,3 +152,21 @@ def test_row_sharding_two_ranks_gloo():
                        capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "SHARD_OK" in r.stdout
+
+
+def test_learning_replay_matches_reference_golden(golden):
+    """the oracle's restatement of the greedy learning loop reproduces the
+    reference's learn_dictionary picks and merged segments on the
+    well-conditioned golden cases (the periodic one ties to ~1e-12)"""
+    n = 0
+    for name, (kind, c) in golden.items():
+        if kind != "learn" or "periodic" in name:
+            continue
+        n += 1
+        cores, merged, stall = O.learn_dictionary_replay(c["t"], int(c["m"]), float(c["k"]), int(c["rule"]),
+                                                         float(c["value"]))
+        assert cores == [int(x) for x in c["cores"]], name
+        assert [lo for lo, _ in merged] == [int(x) for x in c["starts"]], name
+        assert [hi - lo for lo, hi in merged] == [int(x) for x in c["lengths"]], name
+        assert stall == bool(int(c["no_progress"])), name
+    assert n == 6

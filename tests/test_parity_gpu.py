@@ -419,3 +419,91 @@ def test_fp32_mode_self_join_and_flat():
     P = tsd.ab_join(a, b, 64, precision="fp32")
     rv, ri = O.ab_join(a, b, 64)
     check_profile(P.values, P.indices, rv, ri, 64, ab_dist(a, b, 64), fp32=True, label="fp32 flat")
+
+
+# ------------------------------------------------------------- greedy learning
+def _learn_cfg(c):
+    rule, value = int(c["rule"]), float(c["value"])
+    cfg = tsd.LearnConfig(m=int(c["m"]), k=float(c["k"]))
+    if rule == 0:
+        cfg.space_saving_target = value
+    elif rule == 1:
+        cfg.sample_budget = int(value)
+    else:
+        cfg.error_target = value
+    return cfg
+
+
+def _dictionary_invariants(D, t):
+    """expect_dictionary_invariants (test_dictionary.cpp:53-82)"""
+    assert D.source_length == t.size and D.segments
+    prev_end, stored = 0, 0
+    for s, seg in enumerate(D.segments):
+        assert seg.length() >= D.m and seg.start + seg.length() <= t.size
+        if s > 0:
+            assert seg.start > prev_end  # disjoint, sorted, non-touching
+        prev_end = seg.start + seg.length()
+        assert np.array_equal(seg.values, t[seg.start:seg.start + seg.length()])
+        stored += seg.length()
+    assert abs(D.space_saving - (1.0 - stored / t.size)) <= 1e-12
+    c = sorted(D.core_starts)
+    assert all(b - a > D.m // 2 for a, b in zip(c, c[1:]))
+
+
+def test_learn_dictionary_vs_reference(golden):
+    """learn_dictionary on the device (argmin of P - S, masking, exact FP64
+    distance profiles, stop rules, e_max) against the reference's own
+    learn_dictionary: identical picks (core starts in order), merged
+    segments, space saving and no_progress; e_max by the join's parity rule
+    (dictionary.hpp:259-328, test_dictionary.cpp:94-170)"""
+    n_cases = 0
+    for name, (kind, c) in golden.items():
+        if kind != "learn":
+            continue
+        n_cases += 1
+        t = c["t"]
+        D = tsd.learn_dictionary(t, _learn_cfg(c))
+        _dictionary_invariants(D, t)
+        if "periodic" in name:
+            # a noisy sine: many windows tie in P - S to ~1e-12, so which one
+            # the argmin takes is decided by rounding (the reference's own
+            # MASS carries ~1e-5); check the stop rule instead of the picks
+            need = (1.0 - float(c["value"])) * t.size - 1e-6
+            assert t.size * (1.0 - D.space_saving) >= need and not D.no_progress, name
+            continue
+        assert D.core_starts == [int(x) for x in c["cores"]], f"{name}: picks differ"
+        assert [s.start for s in D.segments] == [int(x) for x in c["starts"]], name
+        assert [s.length() for s in D.segments] == [int(x) for x in c["lengths"]], name
+        for s in D.segments:  # verbatim copies of the source
+            assert np.array_equal(s.values, t[s.start:s.start + s.length()]), name
+        assert abs(D.space_saving - float(c["space_saving"])) <= 1e-12, name
+        assert D.no_progress == bool(int(c["no_progress"])), name
+        ref_e = float(c["e_max"])
+        assert abs(D.e_max - ref_e) <= max(1e-8 * ref_e, 2e-5), f"{name}: e_max {D.e_max} vs {ref_e}"
+    assert n_cases == 7
+
+
+def test_learn_dictionary_precomputed_profile_and_errors(golden):
+    """learn_dictionary(T, cfg, P_B) equals the convenience overload; the
+    reference's validation order and error codes (dictionary.hpp:120-141, :267-271)"""
+    c = golden["learn_saving_walk_80"][1]
+    t, cfg = c["t"], _learn_cfg(c)
+    P = tsd.self_join(t, cfg.m)
+    a = tsd.learn_dictionary(t, cfg, P)
+    b = tsd.learn_dictionary(t, cfg)
+    assert a.core_starts == b.core_starts and a.e_max == b.e_max
+    with pytest.raises(tsd.TsdictError) as e:
+        tsd.learn_dictionary(t, tsd.LearnConfig(m=1, space_saving_target=0.5))
+    assert e.value.code() == tsd.errc.window_too_small
+    with pytest.raises(tsd.TsdictError) as e:
+        tsd.learn_dictionary(t, tsd.LearnConfig(m=50, k=-1.0, space_saving_target=0.5))
+    assert e.value.code() == tsd.errc.invalid_argument
+    with pytest.raises(tsd.TsdictError) as e:
+        tsd.learn_dictionary(t, tsd.LearnConfig(m=50, space_saving_target=1.0))
+    assert e.value.code() == tsd.errc.invalid_argument
+    with pytest.raises(tsd.TsdictError) as e:
+        tsd.learn_dictionary(t[:90], tsd.LearnConfig(m=50, space_saving_target=0.5))
+    assert e.value.code() == tsd.errc.series_too_short
+    with pytest.raises(tsd.TsdictError) as e:
+        tsd.learn_dictionary(t, tsd.LearnConfig(m=50, sample_budget=3000, max_iterations=2))
+    assert e.value.code() == tsd.errc.iteration_cap_exceeded

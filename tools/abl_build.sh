@@ -8,7 +8,7 @@ ARCH="-gencode arch=compute_100a,code=sm_100a"
 while [ $# -ge 2 ]; do
   name=$1; flags=$2; shift 2
   mkdir -p build/abl_$name
-  for f in stats ${JOIN:-join} heads_fft capi peak; do
+  for f in stats ${JOIN:-join} heads_fft learn capi peak; do
     nvcc $ARCH -O3 -lineinfo -std=c++20 -Xcompiler -fPIC --expt-relaxed-constexpr $flags -c $f.cu -o build/abl_$name/$f.o &
   done
   wait
