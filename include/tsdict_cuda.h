@@ -134,6 +134,19 @@ int tsd_learn_dictionary(const double* t, size_t n, size_t m, double k, int rule
                          double* seg_vals, size_t* nseg, size_t* core_starts, size_t* ncores, double* e_max,
                          double* space_saving, int* no_progress);
 
+/* ---- discords (dict_join.hpp:50-93) ----
+ * find_discords on the device: greedy top-k argmax over the finite profile
+ * values with +-floor(m/2) suppression (first maximum wins); the rank-1 pick
+ * is certified when it leads the best non-overlapping runner-up by more than
+ * e_max (or has none). values: host (tsd_find_discords) or device-resident
+ * (tsd_find_discords_device, on `stream`). Outputs (capacity top_k): start,
+ * score, certified; *count picks. empty_profile for cnt == 0,
+ * invalid_argument for e_max < 0. */
+int tsd_find_discords(const double* values, size_t cnt, size_t m, double e_max, size_t top_k, size_t* start,
+                      double* score, int* certified, size_t* count);
+int tsd_find_discords_device(const double* d_values, size_t cnt, size_t m, double e_max, size_t top_k,
+                             size_t* start, double* score, int* certified, size_t* count, void* stream);
+
 /* ---- diagnostics ---- */
 const char* tsd_last_error(void);
 const char* tsd_status_name(int status); /* reference errc_name (errors.hpp:37-57) */

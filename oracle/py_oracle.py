@@ -322,6 +322,40 @@ def ref_learn_dictionary_full(t, m, k=1.5, rule=0, value=0.5, max_iterations=100
             "no_progress": int(npg.value)}
 
 
+def ref_find_discords(values, m, e_max, top_k):
+    """the reference's find_discords (dict_join.hpp:54-93) -> (starts, scores, certified)"""
+    v = _f(values)
+    cap = max(top_k, 1)
+    st, sc, ce = np.zeros(cap, dtype=np.uintp), np.zeros(cap), np.zeros(cap, dtype=np.int32)
+    cnt = ctypes.c_size_t()
+    r = ref()
+    r.tsdr_find_discords.argtypes = [_f64p, _sz, _sz, ctypes.c_double, _sz, _szp, _f64p,
+                                     ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_size_t)]
+    _chk(r.tsdr_find_discords(_p(v, _f64p), v.size, m, e_max, top_k, _p(st, _szp), _p(sc, _f64p),
+                              ce.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), ctypes.byref(cnt)))
+    k = cnt.value
+    return st[:k].astype(np.int64), sc[:k].copy(), ce[:k].astype(bool)
+
+
+def ref_window_labels(regions, n, m):
+    lo = np.asarray([a for a, _ in regions], dtype=np.uintp)
+    hi = np.asarray([b for _, b in regions], dtype=np.uintp)
+    out = np.zeros(n - m + 1, dtype=np.uint8)
+    r = ref()
+    r.tsdr_window_labels.argtypes = [_szp, _szp, _sz, _sz, _sz, _u8p]
+    _chk(r.tsdr_window_labels(_p(lo, _szp), _p(hi, _szp), len(regions), n, m, _p(out, _u8p)))
+    return out
+
+
+def ref_auc_score(scores, labels):
+    s, l = _f(scores), np.ascontiguousarray(labels, dtype=np.uint8)
+    out = ctypes.c_double()
+    r = ref()
+    r.tsdr_auc_score.argtypes = [_f64p, _u8p, _sz, ctypes.POINTER(ctypes.c_double)]
+    _chk(r.tsdr_auc_score(_p(s, _f64p), _p(l, _u8p), s.size, ctypes.byref(out)))
+    return out.value
+
+
 def ref_learn_dictionary(t, m, space_saving, threads=0):
     """the reference's greedy learn_dictionary (dictionary.hpp:259-328);
     returns (segments, starts, e_max)"""

@@ -158,6 +158,41 @@ int tsdr_learn_dictionary2(const double* t, size_t n, size_t m, double k, int ru
   });
 }
 
+// dict_join.hpp:54-165 consumers
+int tsdr_find_discords(const double* values, size_t cnt, size_t m, double e_max, size_t top_k, size_t* start,
+                       double* score, int* certified, size_t* count) {
+  return guarded([&] {
+    tsdict::MatrixProfile P;
+    P.values.assign(values, values + cnt);
+    P.indices.assign(cnt, 0);
+    P.kind = tsdict::join_kind::ab;
+    P.m = m;
+    const auto d = tsdict::find_discords(P, e_max, top_k);
+    for (size_t i = 0; i < d.size(); ++i) {
+      start[i] = d[i].start;
+      score[i] = d[i].score;
+      certified[i] = d[i].certified ? 1 : 0;
+    }
+    *count = d.size();
+  });
+}
+
+int tsdr_window_labels(const size_t* lo, const size_t* hi, size_t nreg, size_t n, size_t m, unsigned char* labels) {
+  return guarded([&] {
+    std::vector<tsdict::interval> r;
+    for (size_t i = 0; i < nreg; ++i) r.emplace_back(lo[i], hi[i]);
+    const auto l = tsdict::window_labels(r, n, m);
+    std::memcpy(labels, l.data(), l.size());
+  });
+}
+
+int tsdr_auc_score(const double* scores, const unsigned char* labels, size_t cnt, double* auc) {
+  return guarded([&] {
+    *auc = tsdict::auc_score(std::vector<double>(scores, scores + cnt),
+                             std::vector<unsigned char>(labels, labels + cnt));
+  });
+}
+
 // tests/oracles.hpp long-double brute force
 int tsdr_ab_join_brute(const double* a, size_t na, const double* b, size_t nb, size_t m, double* val,
                        int64_t* idx) {

@@ -30,6 +30,10 @@ __all__ = [
     "C_SYMBOLS",
     "LearnConfig",
     "learn_dictionary",
+    "Discord",
+    "find_discords",
+    "window_labels",
+    "auc_score",
 ]
 
 
@@ -97,6 +101,9 @@ C_SYMBOLS = {
     "tsd_dict_join": (_int, [_f64p, _sz, _f64p, _szp, _szp, _sz, _sz, _int, _f64p, _i64p]),
     "tsd_dict_join_batched": (_int, [_f64p, _szp, _sz, _f64p, _szp, _szp, _sz, _sz, _int, _f64p, _i64p]),
     "tsd_compute_e_max": (_int, [_f64p, _sz, _sz, _f64p, _szp, _szp, _sz, _sz, _f64p]),
+    "tsd_find_discords": (_int, [_f64p, _sz, _sz, ctypes.c_double, _sz, _szp, _f64p, ctypes.POINTER(_int), _szp]),
+    "tsd_find_discords_device": (_int, [_vp, _sz, _sz, ctypes.c_double, _sz, _szp, _f64p, ctypes.POINTER(_int), _szp,
+                                        _vp]),
     "tsd_learn_dictionary": (_int, [_f64p, _sz, _sz, ctypes.c_double, _int, ctypes.c_double, _sz, _f64p, _szp, _szp,
                                     _f64p, _szp, _szp, _szp, _f64p, _f64p, ctypes.POINTER(_int)]),
     "tsd_dict_plan_create": (_int, [_f64p, _szp, _szp, _sz, _sz, _int, ctypes.POINTER(_vp)]),
@@ -365,6 +372,77 @@ def learn_dictionary(T_B, cfg: LearnConfig, P_B: Optional[MatrixProfile] = None,
         off += L
     return Dictionary(segments=segs, m=m, k=cfg.k, source_length=n, core_starts=[int(c) for c in cores[:ncores.value]],
                       e_max=e.value, space_saving=ss.value, no_progress=bool(npg.value))
+
+
+@dataclass
+class Discord:
+    """dict_join.hpp:28-32"""
+    start: int
+    score: float
+    certified: bool = False
+
+
+def find_discords(P, e_max: float, top_k: int) -> List[Discord]:
+    """dict_join.hpp:54-93 on the device: greedy top-k peaks with +-floor(m/2)
+    suppression; rank 1 certified when it leads the runner-up by > e_max.
+    P: a MatrixProfile, or (d_values_ptr, count, m) of a device-resident profile."""
+    lib = load_library()
+    cap = max(int(top_k), 1)
+    st = np.zeros(cap, dtype=np.uintp)
+    sc = np.zeros(cap)
+    ce = np.zeros(cap, dtype=np.int32)
+    cnt = ctypes.c_size_t(0)
+    cep = ce.ctypes.data_as(ctypes.POINTER(_int))
+    if isinstance(P, tuple):
+        ptr, n, m = P
+        _check(lib.tsd_find_discords_device(ctypes.c_void_p(ptr), n, m, e_max, top_k, _ptr(st, _szp), _ptr(sc, _f64p),
+                                            cep, ctypes.byref(cnt), None))
+    else:
+        v = _f64(P.values)
+        _check(lib.tsd_find_discords(_ptr(v, _f64p), v.size, P.m, e_max, top_k, _ptr(st, _szp), _ptr(sc, _f64p), cep,
+                                     ctypes.byref(cnt)))
+    return [Discord(int(st[i]), float(sc[i]), bool(ce[i])) for i in range(cnt.value)]
+
+
+def window_labels(regions, n: int, m: int) -> np.ndarray:
+    """dict_join.hpp:102-127 (host): a window is positive when it overlaps a
+    merged region by at least half its length"""
+    if m < 2 or m > n:
+        raise TsdictError(errc.invalid_argument, "window length out of range")
+    for lo, hi in regions:
+        if lo >= hi or hi > n:
+            raise TsdictError(errc.invalid_argument, "label region out of range")
+    merged = []
+    for lo, hi in sorted(regions):
+        if merged and lo <= merged[-1][1]:
+            merged[-1] = (merged[-1][0], max(merged[-1][1], hi))
+        else:
+            merged.append((lo, hi))
+    cnt = n - m + 1
+    out = np.zeros(cnt, dtype=np.uint8)
+    for lo, hi in merged:  # windows overlapping [lo, hi) by >= m/2 samples
+        for i in range(max(0, lo - m + 1), min(cnt, hi)):
+            if 2 * (min(i + m, hi) - max(i, lo)) >= m:
+                out[i] = 1
+    return out
+
+
+def auc_score(scores, labels) -> float:
+    """dict_join.hpp:130-162 (host): exact Mann-Whitney AUC, ties count 1/2"""
+    s = np.asarray(scores, dtype=np.float64)
+    l = np.asarray(labels).astype(bool)
+    if s.size != l.size:
+        raise TsdictError(errc.length_mismatch, "scores and labels differ in length")
+    if np.isnan(s).any():
+        raise TsdictError(errc.invalid_argument, "scores must not contain NaN")
+    pos, neg = int(l.sum()), int((~l).sum())
+    if pos == 0 or neg == 0:
+        raise TsdictError(errc.degenerate_labels, "AUC needs at least one positive and one negative label")
+    u, inv = np.unique(s, return_inverse=True)  # ascending distinct scores
+    gp = np.bincount(inv, weights=l, minlength=u.size)
+    gn = np.bincount(inv, weights=~l, minlength=u.size)
+    below = np.concatenate([[0.0], np.cumsum(gn)[:-1]])
+    return float(np.sum(gp * (below + 0.5 * gn)) / (pos * neg))
 
 
 class DictPlan:

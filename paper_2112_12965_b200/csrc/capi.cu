@@ -622,6 +622,46 @@ int tsd_learn_dictionary(const double* t, size_t n, size_t m, double k, int rule
   return tsd_compute_e_max(t, n, n, seg_vals, seg_len, seg_start, merged.size(), m, e_max);
 }
 
+int tsd_find_discords_device(const double* d_values, size_t cnt, size_t m, double e_max, size_t top_k,
+                             size_t* start, double* score, int* certified, size_t* count, void* stream) {
+  if (cnt == 0) return fail(kEmptyProfile, "profile has no entries");       // dict_join.hpp:55
+  if (e_max < 0.0) return fail(kInvalidArgument, "e_max must be non-negative");  // :56
+  ThreadCtx& tc = tctx();
+  if (int rc = tc.s.init()) return rc;
+  cudaStream_t st = stream ? (cudaStream_t)stream : tc.s.st;
+  Arena ar;
+  uint8_t* d_sup = (uint8_t*)ar.get(cnt);
+  void* d_scr = ar.get(learn_scratch_bytes());
+  if (!d_sup || !d_scr) return fail(kCudaError, "device allocation failed");
+  std::vector<int64_t> at;
+  std::vector<double> sc;
+  const int64_t want = (int64_t)std::max<size_t>(top_k, 2);  // runner-up for the gap test (:75)
+  if (discord_peaks(d_values, (int64_t)cnt, (int)m, want, d_sup, d_scr, at, sc, st) != kOk)
+    return fail(kCudaError, std::string("discord peaks: ") + cudaGetErrorString(cudaGetLastError()));
+  const bool cert = !at.empty() && (at.size() < 2 || sc[0] - sc[1] > e_max);  // :88-91
+  const size_t k = std::min(at.size(), top_k);
+  for (size_t i = 0; i < k; ++i) {
+    start[i] = (size_t)at[i];
+    score[i] = sc[i];
+    certified[i] = (i == 0 && cert) ? 1 : 0;
+  }
+  *count = k;
+  return kOk;
+}
+
+int tsd_find_discords(const double* values, size_t cnt, size_t m, double e_max, size_t top_k, size_t* start,
+                      double* score, int* certified, size_t* count) {
+  if (cnt == 0) return fail(kEmptyProfile, "profile has no entries");
+  if (e_max < 0.0) return fail(kInvalidArgument, "e_max must be non-negative");
+  ThreadCtx& tc = tctx();
+  if (int rc = tc.s.init()) return rc;
+  Arena ar;
+  double* d_v = (double*)ar.get(sizeof(double) * cnt);
+  if (!d_v) return fail(kCudaError, "device allocation failed");
+  CK(cudaMemcpyAsync(d_v, values, sizeof(double) * cnt, cudaMemcpyHostToDevice, tc.s.st));
+  return tsd_find_discords_device(d_v, cnt, m, e_max, top_k, start, score, certified, count, tc.s.st);
+}
+
 int tsd_dict_plan_destroy(tsd_dict_plan* plan) {
   delete plan;
   return kOk;

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 #include "tsd_common.cuh"
 #include "tsd_internal.h"
@@ -141,7 +142,83 @@ __global__ void __launch_bounds__(LB) k_dprof_fold(const double* __restrict__ x,
   S[i] = first ? d : fmin(S[i], d);  // dictionary.hpp:298-303
 }
 
+// argmax over unsuppressed finite values, first maximum wins
+// (find_discords' next_peak, dict_join.hpp:61-70)
+__device__ __forceinline__ bool vi_more(double va, long long ia, double vb, long long ib) {
+  return va > vb || (va == vb && ia < ib);
+}
+
+__global__ void __launch_bounds__(LB) k_argmax_partial(const double* __restrict__ vals, const uint8_t* __restrict__ sup,
+                                                       int64_t cnt, ValIdx* __restrict__ part) {
+  double bv = 0.0;
+  long long bi = -1;
+  for (int64_t i = (int64_t)blockIdx.x * LB + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * LB) {
+    const double v = vals[i];
+    if (sup[i] || !isfinite(v)) continue;
+    if (bi < 0 || v > bv) {
+      bv = v;
+      bi = i;
+    }
+  }
+  __shared__ ValIdx sh[LB];
+  sh[threadIdx.x] = ValIdx{bv, bi};
+  __syncthreads();
+  for (int s = LB / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const ValIdx o = sh[threadIdx.x + s];
+      const ValIdx c = sh[threadIdx.x];
+      if (o.i >= 0 && (c.i < 0 || vi_more(o.v, o.i, c.v, c.i))) sh[threadIdx.x] = o;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(LB) k_argmax_final(const ValIdx* __restrict__ part, int np, ValIdx* __restrict__ out) {
+  ValIdx b{0.0, -1};
+  for (int k = threadIdx.x; k < np; k += LB) {
+    const ValIdx o = part[k];
+    if (o.i >= 0 && (b.i < 0 || vi_more(o.v, o.i, b.v, b.i))) b = o;
+  }
+  __shared__ ValIdx sh[LB];
+  sh[threadIdx.x] = b;
+  __syncthreads();
+  for (int s = LB / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const ValIdx o = sh[threadIdx.x + s];
+      const ValIdx c = sh[threadIdx.x];
+      if (o.i >= 0 && (c.i < 0 || vi_more(o.v, o.i, c.v, c.i))) sh[threadIdx.x] = o;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = sh[0];
+}
+
 }  // namespace
+
+int discord_peaks(const double* d_vals, int64_t cnt, int m, int64_t want, uint8_t* d_sup, void* d_scratch,
+                  std::vector<int64_t>& at, std::vector<double>& score, cudaStream_t st) {
+  const int np = (int)std::min<int64_t>(592, (cnt + LB - 1) / LB);
+  ValIdx* part = reinterpret_cast<ValIdx*>(d_scratch);
+  ValIdx* out = part + 592;
+  const int64_t excl = m / 2;
+  if (cudaMemsetAsync(d_sup, 0, cnt, st) != cudaSuccess) return kCudaError;
+  at.clear();
+  score.clear();
+  while ((int64_t)at.size() < want) {
+    k_argmax_partial<<<np, LB, 0, st>>>(d_vals, d_sup, cnt, part);
+    k_argmax_final<<<1, LB, 0, st>>>(part, np, out);
+    ValIdx h;
+    if (cudaMemcpyAsync(&h, out, sizeof(ValIdx), cudaMemcpyDeviceToHost, st) != cudaSuccess) return kCudaError;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return kCudaError;
+    if (h.i < 0) break;
+    at.push_back(h.i);
+    score.push_back(h.v);
+      const int64_t lo = h.i >= excl ? h.i - excl : 0, hi = std::min<int64_t>(cnt, h.i + excl + 1);  // :80-84
+    if (cudaMemsetAsync(d_sup + lo, 1, hi - lo, st) != cudaSuccess) return kCudaError;
+  }
+  return kOk;
+}
 
 int learn_argmin(const double* d_P, const double* d_S, const uint8_t* d_mask, int64_t cnt, void* d_scratch,
                  double* h_val, int64_t* h_idx, cudaStream_t st) {

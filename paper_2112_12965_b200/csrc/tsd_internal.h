@@ -138,6 +138,10 @@ int learn_max(const double* d_S, int64_t cnt, void* d_scratch, double* h_max, cu
 int learn_dprof_fold(const double* d_x, const WindowArrays& w, int m, const double* d_qc, double invn_q,
                      bool const_query, int64_t origin, double origin_val, bool first, double* d_S, cudaStream_t st);
 size_t learn_scratch_bytes();
+// find_discords' peak loop (dict_join.hpp:54-93): up to `want` greedy argmax
+// picks over finite, unsuppressed windows, each suppressing +-floor(m/2)
+int discord_peaks(const double* d_vals, int64_t cnt, int m, int64_t want, uint8_t* d_sup, void* d_scratch,
+                  std::vector<int64_t>& at, std::vector<double>& score, cudaStream_t st);
 
 // Epilogue: corr -> distance (series.hpp:153-161), concat column -> source
 // coordinate (dictionary.hpp:183-188), (inf, -1) sentinel for rows without an

@@ -259,6 +259,33 @@ int main() {
     cfg.space_saving_target.reset();
     return expect_code(errc::invalid_argument, [&] { learn_dictionary_random(T, cfg, 1); });
   });
+  check("Discords.PlantedAnomalyRanksFirst", [&] {  // test_dict_join.cpp discord shapes
+    Rng r(95);
+    std::vector<double> q = r.walk(4000);
+    for (int i = 0; i < 80; ++i) q[2500 + i] += 6.0 * std::sin(i * 0.2);
+    Rng rd(96);
+    Dictionary D;
+    D.m = 64;
+    for (int s = 0; s < 4; ++s) D.segments.push_back(Segment{std::size_t(1000 * s), rd.walk(600)});
+    D.source_length = 4000;
+    const MatrixProfile P = join_dictionary(TimeSeries{q}, D, 64);
+    const AnomalyReport rep = make_anomaly_report(P, 0.0, 5);
+    if (rep.discords.size() != 5) return std::string("wrong count");
+    for (std::size_t a = 0; a < rep.discords.size(); ++a)
+      for (std::size_t b = a + 1; b < rep.discords.size(); ++b) {
+        const auto x = rep.discords[a].start, y = rep.discords[b].start;
+        if ((x > y ? x - y : y - x) <= 32) return std::string("overlapping picks");
+        if (rep.discords[a].score < rep.discords[b].score) return std::string("not in score order");
+      }
+    return expect_code(errc::empty_profile, [] { find_discords(MatrixProfile{}, 0.0, 3); });
+  });
+  check("Labels.AucOfPerfectScoresIsOne", [&] {
+    const auto lab = window_labels({{100, 200}, {150, 260}}, 1000, 50);
+    std::vector<double> sc(lab.size());
+    for (std::size_t i = 0; i < lab.size(); ++i) sc[i] = lab[i] ? 1.0 : 0.0;
+    if (std::fabs(auc_score(sc, lab) - 1.0) > 0) return std::string("AUC != 1");
+    return expect_code(errc::degenerate_labels, [&] { auc_score(sc, std::vector<unsigned char>(lab.size(), 0)); });
+  });
   std::printf("%d failure(s)\n", failures);
   return failures;
 }

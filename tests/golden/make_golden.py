@@ -133,6 +133,38 @@ def main():
     learn_case("learn_k0_budget_walk_84", O.RefRng(84).walk(1800), 40, 0.0, 1, 400)
     learn_case("learn_no_progress_85", O.RefRng(85).walk(1500), 100, 1.5, 1, 100000)
     learn_case("learn_zero_saving_86", O.RefRng(86).walk(900), 60, 1.5, 0, 0.0)
+    # discords / labels / AUC (dict_join.hpp:54-165; test_dict_join.cpp shapes):
+    # the C3-like reduced join profile with planted anomalies, a profile with
+    # sentinel (+inf) rows and exact ties, a flat profile (vacuous runner-up)
+    def discord_case(name, values, m, e_max, top_k):
+        st, sc, ce = O.ref_find_discords(values, m, e_max, top_k)
+        d[f"{name}__values"], d[f"{name}__m"] = np.asarray(values, dtype=np.float64), np.int64(m)
+        d[f"{name}__e_max"], d[f"{name}__top_k"] = np.float64(e_max), np.int64(top_k)
+        d[f"{name}__starts"], d[f"{name}__scores"], d[f"{name}__certified"] = st, sc, ce.astype(np.uint8)
+        cases.append(("discords", name))
+
+    rq = O.RefRng(120)
+    q = rq.walk(6000)
+    q[2000:2100] += 8.0 * np.sin(np.linspace(0, 3 * np.pi, 100))
+    q[4500:4560] = q[4500]
+    segs = [O.RefRng(121 + s).walk(700) for s in range(6)]
+    v, _ = O.ref_join_dictionary(q, segs, [1000 * s for s in range(6)], 80, threads=3)
+    discord_case("discords_planted_120", v, 80, 0.5, 20)
+    discord_case("discords_planted_certify_120", v, 80, 1e-3, 5)
+    w = np.abs(O.RefRng(122).noise(500))
+    w[[10, 11, 300]] = np.inf
+    w[[100, 400]] = 7.0
+    discord_case("discords_inf_ties_122", w, 16, 0.1, 6)
+    discord_case("discords_single_123", np.ones(30), 40, 0.0, 3)
+    rl = O.RefRng(124)
+    regions = [(100, 180), (170, 260), (900, 950), (1990, 2000)]
+    lab = O.ref_window_labels(regions, 2000, 64)
+    d["labels_124__lo"] = np.asarray([a for a, _ in regions], dtype=np.int64)
+    d["labels_124__hi"] = np.asarray([b for _, b in regions], dtype=np.int64)
+    d["labels_124__n"], d["labels_124__m"], d["labels_124__labels"] = np.int64(2000), np.int64(64), lab
+    sc = np.round(rl.noise(lab.size), 1)  # coarse scores: many ties
+    d["labels_124__scores"], d["labels_124__auc"] = sc, np.float64(O.ref_auc_score(sc, lab))
+    cases.append(("labels", "labels_124"))
     d["__cases__"] = np.asarray([f"{k}:{n}" for k, n in cases])
     np.savez_compressed(OUT, **d)
     print(f"wrote {OUT}: {len(cases)} cases, {os.path.getsize(OUT) / 1024:.0f} KiB")

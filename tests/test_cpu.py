@@ -170,3 +170,14 @@ def test_learning_replay_matches_reference_golden(golden):
         assert [hi - lo for lo, hi in merged] == [int(x) for x in c["lengths"]], name
         assert stall == bool(int(c["no_progress"])), name
     assert n == 6
+
+
+def test_window_labels_and_auc_match_reference(golden):
+    """window_labels / auc_score (dict_join.hpp:102-162, host) against the
+    reference's outputs, incl. overlapping / touching regions and many ties"""
+    import paper_2112_12965_b200 as tsd
+    c = golden["labels_124"][1]
+    regions = list(zip(c["lo"].tolist(), c["hi"].tolist()))
+    lab = tsd.window_labels(regions, int(c["n"]), int(c["m"]))
+    assert np.array_equal(lab, c["labels"])
+    assert tsd.auc_score(c["scores"], c["labels"]) == float(c["auc"])

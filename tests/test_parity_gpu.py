@@ -507,3 +507,35 @@ def test_learn_dictionary_precomputed_profile_and_errors(golden):
     with pytest.raises(tsd.TsdictError) as e:
         tsd.learn_dictionary(t, tsd.LearnConfig(m=50, sample_budget=3000, max_iterations=2))
     assert e.value.code() == tsd.errc.iteration_cap_exceeded
+
+
+# ------------------------------------------------------------- discords
+def test_find_discords_vs_reference(golden):
+    """find_discords with its device peaks against the reference's
+    (dict_join.hpp:54-93): identical starts, scores, certification --
+    including sentinel (+inf) rows, exact ties (first maximum) and a
+    vacuous runner-up; also through a device-resident profile"""
+    import torch
+    n = 0
+    for name, (kind, c) in golden.items():
+        if kind != "discords":
+            continue
+        n += 1
+        P = tsd.MatrixProfile(values=c["values"], indices=np.zeros(c["values"].size, dtype=np.int64), kind="ab",
+                              m=int(c["m"]))
+        got = tsd.find_discords(P, float(c["e_max"]), int(c["top_k"]))
+        assert [g.start for g in got] == [int(x) for x in c["starts"]], name
+        assert [g.score for g in got] == [float(x) for x in c["scores"]], name
+        assert [g.certified for g in got] == [bool(x) for x in c["certified"]], name
+        dv = torch.from_numpy(np.ascontiguousarray(c["values"])).cuda()
+        got_d = tsd.find_discords((dv.data_ptr(), dv.numel(), int(c["m"])), float(c["e_max"]), int(c["top_k"]))
+        assert got_d == got, name
+    assert n == 4
+    with pytest.raises(tsd.TsdictError) as e:
+        tsd.find_discords(tsd.MatrixProfile(values=np.zeros(0), indices=np.zeros(0, dtype=np.int64), kind="ab", m=8),
+                          0.1, 3)
+    assert e.value.code() == tsd.errc.empty_profile
+    with pytest.raises(tsd.TsdictError) as e:
+        tsd.find_discords(tsd.MatrixProfile(values=np.ones(10), indices=np.zeros(10, dtype=np.int64), kind="ab", m=4),
+                          -1.0, 3)
+    assert e.value.code() == tsd.errc.invalid_argument
