@@ -273,11 +273,14 @@ def run_gpu(args):
     # sanity: the e2e result equals the device-resident result
     same = bool(torch.equal(h_idx, d_idx.cpu())) and bool(torch.equal(h_val, d_val.cpu()))
 
+    sj = self_join_lines(q, dist, world)  # every rank (the sharded run needs all of them)
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return 0
     peak = tsd.measure_peak("fp64", seconds=2.0)
+    for v in sj.values():  # against the FP64 cell peak of the GPUs used
+        v["frac_of_fp64_cell_peak"] = v["value"] * 1e9 / (v.get("n_gpus", 1) * peak / FLOPS_PER_CELL)
     jms = statistics.median(join_ms)
     kms = statistics.median(kernel_ms)
     hms = statistics.median(heads_ms)
@@ -306,7 +309,7 @@ def run_gpu(args):
                     "d2h_bytes_per_step": int(nrows * 16), "api": "tsd_dict_join (host buffers, pinned)",
                     "matches_device_path": same},
             "gpu_launches": launches, "clocks": clk.summary(),
-            "self_join": self_join_lines(q, peak),
+            "self_join": sj,
             "join_ms_median": jms, "fraction_of_fp64_peak_cells": (cells_per_step() / (jms * 1e-3)) /
                                                                     (peak / FLOPS_PER_CELL)}
     print(json.dumps(line), flush=True)
@@ -315,16 +318,41 @@ def run_gpu(args):
     return 0
 
 
-def self_join_lines(q, peak):
+def self_join_lines(q, dist=None, world=1):
     """Self-join throughput in the reference's unit (one admissible unordered
     pair |i - j| > excl evaluated once, profiles.hpp:287-297):
     the SURVEY's proposed target (a 2^21 prefix of the C4 query, m = 512,
     excl = m/2) and BASELINE C2 (ECG-like, n = 131072, m = 250, excl = m/4).
-    Host API (tsd_self_join), so host<->device copies are inside the time."""
+    Host API (tsd_self_join), so host<->device copies are inside the time.
+    N > 1 (torchrun): the sharded self-join over all ranks -- strong scaling,
+    one all-gather of per-row partials, max-over-ranks time. Call on every
+    rank; the frac fields are added by the caller."""
     import torch
     import paper_2112_12965_b200 as tsd
     from paper_2112_12965_b200 import synth
     out = {}
+    if dist is not None and world > 1:
+        x = np.ascontiguousarray(q[: 1 << 21])
+        m = 512
+        cnt, e = x.size - m + 1, m // 2
+        pairs = (cnt - e - 1) * (cnt - e) / 2
+        tsd.self_join_sharded(x, m)  # warm
+        ts = []
+        for _ in range(3):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tsd.self_join_sharded(x, m)
+            torch.cuda.synchronize()
+            t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ts.append(float(t.item()))
+        t = statistics.median(ts)
+        out["self_2^21_m512_sharded"] = {"n": int(x.size), "m": m, "excl": e, "pairs": pairs, "ms": t * 1e3,
+                                         "value": pairs / t / 1e9, "unit": "GPair/s", "n_gpus": world,
+                                         "scaling": "strong",
+                                         "kernel": "symmetric upper-triangle sweep, sharded by task + all-gather"}
+        return out
     for name, x, m, excl in (("self_2^21_m512", np.ascontiguousarray(q[: 1 << 21]), 512, None),
                              ("C2_self_ecg_m250", synth.ecg(2, 131072)[0], 250, 62)):
         cnt = x.size - m + 1
@@ -340,7 +368,6 @@ def self_join_lines(q, peak):
         t = statistics.median(ts)
         out[name] = {"n": int(x.size), "m": m, "excl": e, "pairs": pairs, "ms": t * 1e3,
                      "value": pairs / t / 1e9, "unit": "GPair/s",
-                     "frac_of_fp64_cell_peak": pairs / t / (peak / FLOPS_PER_CELL),
                      "kernel": "symmetric upper-triangle sweep" if cnt >= 450000 else "full-matrix sweep"}
     return out
 

@@ -63,6 +63,21 @@ int tsd_ab_join(const double* a, size_t na, const double* b, size_t nb, size_t m
 #define TSD_EXCL_DEFAULT ((size_t)-1)
 int tsd_self_join(const double* t, size_t n, size_t m, size_t excl, int precision, double* val, int64_t* idx);
 
+/* Sharded self-join (multi-GPU): shard s of S sweeps every S-th
+ * task of the symmetric upper-triangle decomposition and returns per-row
+ * partials over ALL rows -- corr (clamped correlation, -2 = none) and col
+ * (window index, -1 = none) -- covering its pairs from both ends. The
+ * exchange is one all-gather of the partials; tsd_profile_merge applies
+ * acc_merge's rule (larger corr, then lower index; profiles.hpp:79-85) and
+ * tsd_self_join_finish turns the merged partials into the profile
+ * (distances, flat rows, sentinel) exactly as tsd_self_join does. */
+int tsd_self_join_partial(const double* t, size_t n, size_t m, size_t excl, size_t shard, size_t nshards,
+                          double* corr, int64_t* col);
+int tsd_profile_merge(const double* corr_parts, const int64_t* col_parts, size_t nparts, size_t cnt, double* corr,
+                      int64_t* col);
+int tsd_self_join_finish(const double* t, size_t n, size_t m, size_t excl, const double* corr, const int64_t* col,
+                         double* val, int64_t* idx);
+
 /* Replaces tsdict::detail::dict_min_profile (dictionary.hpp:149-193), the
  * engine of join_dictionary (dict_join.hpp:42-48) and compute_e_max
  * (dictionary.hpp:247-255). Segments are packed back to back in seg_vals

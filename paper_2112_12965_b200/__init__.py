@@ -32,6 +32,11 @@ __all__ = [
     "learn_dictionary",
     "Discord",
     "find_discords",
+    "self_join_partial",
+    "merge_partials",
+    "self_join_finish",
+    "exchange_partials",
+    "self_join_sharded",
     "window_labels",
     "auc_score",
 ]
@@ -104,6 +109,9 @@ C_SYMBOLS = {
     "tsd_find_discords": (_int, [_f64p, _sz, _sz, ctypes.c_double, _sz, _szp, _f64p, ctypes.POINTER(_int), _szp]),
     "tsd_find_discords_device": (_int, [_vp, _sz, _sz, ctypes.c_double, _sz, _szp, _f64p, ctypes.POINTER(_int), _szp,
                                         _vp]),
+    "tsd_self_join_partial": (_int, [_f64p, _sz, _sz, _sz, _sz, _sz, _f64p, _i64p]),
+    "tsd_profile_merge": (_int, [_f64p, _i64p, _sz, _sz, _f64p, _i64p]),
+    "tsd_self_join_finish": (_int, [_f64p, _sz, _sz, _sz, _f64p, _i64p, _f64p, _i64p]),
     "tsd_learn_dictionary": (_int, [_f64p, _sz, _sz, ctypes.c_double, _int, ctypes.c_double, _sz, _f64p, _szp, _szp,
                                     _f64p, _szp, _szp, _szp, _f64p, _f64p, ctypes.POINTER(_int)]),
     "tsd_dict_plan_create": (_int, [_f64p, _szp, _szp, _sz, _sz, _int, ctypes.POINTER(_vp)]),
@@ -372,6 +380,68 @@ def learn_dictionary(T_B, cfg: LearnConfig, P_B: Optional[MatrixProfile] = None,
         off += L
     return Dictionary(segments=segs, m=m, k=cfg.k, source_length=n, core_starts=[int(c) for c in cores[:ncores.value]],
                       e_max=e.value, space_saving=ss.value, no_progress=bool(npg.value))
+
+
+# --------------------------------------------------------------------------- sharded self-join
+def _excl_arg(m, excl):
+    return ctypes.c_size_t(-1).value if excl is None else int(excl)
+
+
+def self_join_partial(T, m: int, excl: Optional[int] = None, shard: int = 0, nshards: int = 1):
+    """One shard of the symmetric self-join: per-row (corr, window) partials over
+    ALL rows (corr -2 / window -1 = none) for every nshards-th task."""
+    x = _vals(T)
+    cnt = max(1, x.size - m + 1)
+    corr, col = np.empty(cnt), np.empty(cnt, dtype=np.int64)
+    _check(load_library().tsd_self_join_partial(_ptr(x, _f64p), x.size, m, _excl_arg(m, excl), shard, nshards,
+                                                _ptr(corr, _f64p), _ptr(col, _i64p)))
+    return corr, col
+
+
+def merge_partials(corrs, cols):
+    """acc_merge's rule over shards (profiles.hpp:79-85): larger corr, then lower index."""
+    C = np.ascontiguousarray(np.stack([np.asarray(c, dtype=np.float64) for c in corrs]))
+    J = np.ascontiguousarray(np.stack([np.asarray(j, dtype=np.int64) for j in cols]))
+    cnt = C.shape[1]
+    corr, col = np.empty(cnt), np.empty(cnt, dtype=np.int64)
+    _check(load_library().tsd_profile_merge(_ptr(C, _f64p), _ptr(J, _i64p), C.shape[0], cnt, _ptr(corr, _f64p),
+                                            _ptr(col, _i64p)))
+    return corr, col
+
+
+def self_join_finish(T, m: int, excl: Optional[int], corr, col) -> MatrixProfile:
+    """Merged partials -> the self-join profile (distances, flat rows, sentinel)."""
+    x = _vals(T)
+    c, j = _f64(corr), np.ascontiguousarray(col, dtype=np.int64)
+    val, idx = np.empty(c.size), np.empty(c.size, dtype=np.int64)
+    _check(load_library().tsd_self_join_finish(_ptr(x, _f64p), x.size, m, _excl_arg(m, excl), _ptr(c, _f64p),
+                                               _ptr(j, _i64p), _ptr(val, _f64p), _ptr(idx, _i64p)))
+    return MatrixProfile(values=val, indices=idx, kind="self", m=m)
+
+
+def exchange_partials(corr, col, group=None):
+    """The one exchange step of the sharded self-join: all-gather
+    every rank's partials (NCCL has no (max, argmax) reduction) and merge."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    c = torch.from_numpy(np.ascontiguousarray(corr, dtype=np.float64)).to(dev)
+    j = torch.from_numpy(np.ascontiguousarray(col, dtype=np.int64)).to(dev)
+    cs = [torch.empty_like(c) for _ in range(world)]
+    js = [torch.empty_like(j) for _ in range(world)]
+    dist.all_gather(cs, c, group=group)
+    dist.all_gather(js, j, group=group)
+    return merge_partials([x.cpu().numpy() for x in cs], [x.cpu().numpy() for x in js])
+
+
+def self_join_sharded(T, m: int, excl: Optional[int] = None, group=None) -> MatrixProfile:
+    """Self-join over the ranks of a torch.distributed group (one GPU each):
+    shard of the symmetric sweep, one all-gather, merge, finish."""
+    import torch.distributed as dist
+    corr, col = self_join_partial(T, m, excl, dist.get_rank(group), dist.get_world_size(group))
+    corr, col = exchange_partials(corr, col, group)
+    return self_join_finish(T, m, excl, corr, col)
 
 
 @dataclass

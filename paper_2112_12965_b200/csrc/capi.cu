@@ -294,8 +294,12 @@ int tsd_compute_stats(const double* x, size_t n, size_t m, double* means, double
 }
 
 // shared by ab_join and self_join: one series of rows, one segment of columns
+// stage 0: join + epilogue; 1: join only, val/idx receive the raw per-row
+// (corr, column) partials of shard `shard` of `nshards`; 2: epilogue only,
+// val/idx hold merged raw partials on input and the profile on output
 static int single_join(const double* a, size_t na, const double* b, size_t nb, size_t m, int64_t excl, int precision,
-                       double* val, int64_t* idx, bool force_sym = false) {
+                       double* val, int64_t* idx, bool force_sym = false, int stage = 0, int shard = 0,
+                       int nshards = 1) {
   ThreadCtx& tc = tctx();
   if (int rc = tc.s.init()) return rc;
   tc.arena.reset();
@@ -310,6 +314,8 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
   Error er{0, ""};
   JoinInputs in;
   in.force_sym = force_sym;
+  in.shard = shard;
+  in.nshards = nshards;
   std::vector<Group> ga;
   add_groups(ga, 0, (int64_t)na, (int)m, 0, 0);
   int bad = -1;
@@ -340,7 +346,18 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
   if (!d_bc || !d_bj || !d_val || !d_idx || !d_segs) return fail(kCudaError, "device allocation failed");
   CK(cudaMemcpyAsync(d_segs, in.segs.data(), sizeof(SegDev), cudaMemcpyHostToDevice, st));
   int launches = 0;
-  TRY(run_join(in, d_bc, d_bj, tc.arena, st, &er, &launches));
+  if (stage == 2) {
+    CK(cudaMemcpyAsync(d_bc, val, sizeof(double) * nrows, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_bj, idx, sizeof(int64_t) * nrows, cudaMemcpyHostToDevice, st));
+  } else {
+    TRY(run_join(in, d_bc, d_bj, tc.arena, st, &er, &launches));
+  }
+  if (stage == 1) {
+    CK(cudaMemcpyAsync(val, d_bc, sizeof(double) * nrows, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(idx, d_bj, sizeof(int64_t) * nrows, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return kOk;
+  }
   TRY(run_epilogue(d_bc, d_bj, in.rows.flag, nrows, d_segs, 1, (int)m, nullptr, nullptr, 1, in.cols.flag, in.cols.nwin,
                    excl, d_val, d_idx, tc.arena, st, &er));
   CK(cudaMemcpyAsync(val, d_val, sizeof(double) * nrows, cudaMemcpyDeviceToHost, st));
@@ -363,6 +380,45 @@ int tsd_self_join(const double* t, size_t n, size_t m, size_t excl, int precisio
   if (precision != TSD_FP64 && precision != TSD_FP32) return fail(kInvalidArgument, "unknown precision");
   const int64_t e = excl == TSD_EXCL_DEFAULT ? (int64_t)(m / 2) : (int64_t)excl;  // :273
   return single_join(t, n, nullptr, 0, m, e, precision, val, idx);
+}
+
+int tsd_self_join_partial(const double* t, size_t n, size_t m, size_t excl, size_t shard, size_t nshards,
+                          double* corr, int64_t* col) {
+  if (m >= 2 && n < 2 * m) return fail(kSeriesTooShort, "self-join needs n >= 2m");
+  if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");
+  if (nshards == 0 || shard >= nshards) return fail(kInvalidArgument, "shard index out of range");
+  const int64_t e = excl == TSD_EXCL_DEFAULT ? (int64_t)(m / 2) : (int64_t)excl;
+  return single_join(t, n, nullptr, 0, m, e, TSD_FP64, corr, col, true, 1, (int)shard, (int)nshards);
+}
+
+int tsd_profile_merge(const double* corr_parts, const int64_t* col_parts, size_t nparts, size_t cnt, double* corr,
+                      int64_t* col) {
+  for (size_t i = 0; i < cnt; ++i) {  // acc_merge (profiles.hpp:79-85): larger corr, then lower index
+    double bc = -2.0;
+    int64_t bj = -1;
+    for (size_t p = 0; p < nparts; ++p) {
+      const double c = corr_parts[p * cnt + i];
+      const int64_t j = col_parts[p * cnt + i];
+      if (j >= 0 && (bj < 0 || c > bc || (c == bc && j < bj))) {
+        bc = c;
+        bj = j;
+      }
+    }
+    corr[i] = bc;
+    col[i] = bj;
+  }
+  return kOk;
+}
+
+int tsd_self_join_finish(const double* t, size_t n, size_t m, size_t excl, const double* corr, const int64_t* col,
+                         double* val, int64_t* idx) {
+  if (m >= 2 && n < 2 * m) return fail(kSeriesTooShort, "self-join needs n >= 2m");
+  if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");
+  const int64_t e = excl == TSD_EXCL_DEFAULT ? (int64_t)(m / 2) : (int64_t)excl;
+  const size_t cnt = n - m + 1;
+  std::copy(corr, corr + cnt, val);
+  std::copy(col, col + cnt, idx);
+  return single_join(t, n, nullptr, 0, m, e, TSD_FP64, val, idx, true, 2);
 }
 
 int tsd_dict_join(const double* q, size_t nq, const double* seg_vals, const size_t* seg_len, const size_t* seg_start,

@@ -1487,7 +1487,10 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
         best = mk;
         bbest = bp;
         sym_tasks.clear();
-        for (const auto& c : cand) sym_tasks.push_back(c.second);
+        // sharded (multi-GPU) self-join: every nshards-th task of the
+        // longest-first order, so each shard gets an even share of the cells
+        for (size_t q = 0; q < cand.size(); ++q)
+          if ((int)(q % (size_t)in.nshards) == in.shard) sym_tasks.push_back(cand[q].second);
       }
     }
     bpt = bbest;

@@ -103,6 +103,7 @@ struct JoinInputs {
   int64_t excl = -1;  // self-join exclusion half-width (|i-j| <= excl rejected); -1 = AB join
   int precision;      // 0 fp64, 1 fp32
   bool force_sym = false;  // self-join: the symmetric sweep at any size (bitwise-equal pair values)
+  int shard = 0, nshards = 1;  // symmetric self-join: this call sweeps every nshards-th task from `shard`
   // optional timing events: [0, 1] around the FFT heads pre-pass, [2, 3]
   // around the join kernel (recorded when non-null); heads_used set by run_join
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};

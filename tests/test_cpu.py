@@ -181,3 +181,14 @@ def test_window_labels_and_auc_match_reference(golden):
     lab = tsd.window_labels(regions, int(c["n"]), int(c["m"]))
     assert np.array_equal(lab, c["labels"])
     assert tsd.auc_score(c["scores"], c["labels"]) == float(c["auc"])
+
+
+def test_sharded_self_join_exchange_two_ranks_gloo():
+    """the sharded self-join's exchange step (all-gather of per-row partials +
+    acc_merge through the C ABI's tsd_profile_merge) over a world_size-2 gloo
+    group reproduces the single-rank result; partials from a numpy brute force"""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(30500 + os.getpid() % 1000))
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_selfshard_worker.py")], env=env,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "SELFSHARD_OK" in r.stdout

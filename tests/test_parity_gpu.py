@@ -539,3 +539,18 @@ def test_find_discords_vs_reference(golden):
         tsd.find_discords(tsd.MatrixProfile(values=np.ones(10), indices=np.zeros(10, dtype=np.int64), kind="ab", m=4),
                           -1.0, 3)
     assert e.value.code() == tsd.errc.invalid_argument
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_sharded_self_join_equals_unsharded(monkeypatch, nshards):
+    """every shard of the symmetric self-join computed in turn on one GPU,
+    merged and finished, equals the unsharded symmetric self-join bitwise
+    (same task decomposition, each task in exactly one shard)"""
+    monkeypatch.setenv("TSD_SYM", "1")
+    t = synth.walk(61, 70000)
+    m = 128
+    ref = tsd.self_join(t, m)
+    parts = [tsd.self_join_partial(t, m, None, s, nshards) for s in range(nshards)]
+    corr, col = tsd.merge_partials([p[0] for p in parts], [p[1] for p in parts])
+    P = tsd.self_join_finish(t, m, None, corr, col)
+    assert np.array_equal(P.indices, ref.indices) and np.array_equal(P.values, ref.values)
