@@ -45,7 +45,7 @@ namespace tsd {
 namespace {
 
 constexpr int WARPS = 2;  // warps per CTA (independent; small CTAs give finer occupancy steps)
-constexpr int T = 128;    // head staging chunk (samples)
+constexpr int T = 64;     // head / top-edge staging chunk (samples)
 #ifndef TSD_JOIN_MINB
 #define TSD_JOIN_MINB 8  // 8 CTAs x 2 warps per SM: caps registers at 128
 #endif
@@ -106,6 +106,14 @@ struct __align__(16) WarpSmem {
   double4 colbuf[3][32];
   double ering[96];
   double cring[96];   // SYM: column thresholds (cthr snapshot), same ring layout as ering
+  double inva[R][32];  // SYM: invn_a of each slot's row (column-side candidates)
+  // SYM: column candidates found since the last chunk turn ({order key, row,
+  // col}; at most 40: a segment's last chunk has no turn), merged into ccand
+  // at the next turn or at the segment end, one lane per entry
+  unsigned long long cq_key[48];
+  unsigned cq_row[48];
+  int cq_col[48];
+  int cq_n;
   double bK[R][32];  // best K = cov * invn_b per slot (row factor invn_a left out); +inf = inactive row
   int bj[R][32];     // its concatenated column
   double slide[Geo<R>::SLIDE];
@@ -342,9 +350,9 @@ __device__ __forceinline__ void cas128(unsigned long long* p, unsigned long long
 // vals: the lane's 8 slot covariances at column col (shared memory [8][32]);
 // cm: slots that passed the column threshold. The warp's lexicographic best (max corr, lowest row) is found
 // with three REDUX reductions on the order key and the row.
-__device__ __noinline__ void col_update(const double* vals, const double* __restrict__ invn_a, int lane,
-                                        unsigned cm, long long row0, long long col, double invb, long long excl,
-                                        long long nrows, unsigned long long* ccand, double* cthr) {
+template <int R>
+__device__ __noinline__ void col_update(WarpSmem<R>& sm, const double* vals, int lane, unsigned cm, long long row0,
+                                        long long col, double invb, long long excl, double* cthr) {
   unsigned long long bk = 0;  // order key of the lane's best corr (0 = none)
   unsigned brow = 0xffffffffu;
   if (invb > 0.0) {
@@ -352,8 +360,8 @@ __device__ __noinline__ void col_update(const double* vals, const double* __rest
       const int r = __ffs(mm) - 1;
       const long long row = row0 + r;
       const long long d = col - row;
-      const double ia = row < nrows ? invn_a[row] : 0.0;
-      if ((d > excl || d < -excl) && ia > 0.0) {
+      const double ia = sm.inva[r][lane];  // 0 for inactive rows
+      if (ia > 0.0 && (d > excl || d < -excl)) {
         // the same rounding as the row side's clamp((cov * invn_b) * invn_a):
         // both rows of a pair see the bitwise-identical correlation, as in the
         // reference (one value updates both, profiles.hpp:289-296)
@@ -375,21 +383,41 @@ __device__ __noinline__ void col_update(const double* vals, const double* __rest
   if (lane == 0 && wk != 0) atomicAdd(&g_cas_count, 1ull);
 #endif
   if (lane == 0 && wk != 0) {
+    // raise the column threshold now (a real pair's value never exceeds the
+    // row's final best; non-returning atomic) and queue the (corr, row)
+    // candidate for the 128-bit merge at the next chunk turn
+    const double t = kplus_d(key_value(wk)) * (1.0 / invb) * (1.0 - 0x1p-40);
+    atomicMax(reinterpret_cast<long long*>(cthr + col), __double_as_longlong(t));
+    const int q = sm.cq_n;
+    sm.cq_key[q] = wk;
+    sm.cq_row[q] = wrow;
+    sm.cq_col[q] = (int)col;
+    sm.cq_n = q + 1;
+  }
+}
+
+// merge the queued column candidates: one lane per entry, all CAS latencies
+// overlapped
+template <int R>
+__device__ __noinline__ void col_flush(WarpSmem<R>& sm, int lane, unsigned long long* ccand) {
+  __syncwarp();
+  const int nq = sm.cq_n;
+  for (int e = lane; e < nq; e += 32) {
+    const long long col = sm.cq_col[e];
     unsigned long long* p = ccand + 2 * col;
-    const unsigned long long nk = wk, ni = (unsigned long long)wrow;
+    const unsigned long long nk = sm.cq_key[e], ni = sm.cq_row[e];
     unsigned long long ck = p[0], ci = p[1];  // may be torn: the CAS validates
     while (nk > ck || (nk == ck && ni < ci)) {
       unsigned long long ok, oi;
       cas128(p, ck, ci, nk, ni, ok, oi);
-      if (ok == ck && oi == ci) {
-        const double t = kplus_d(key_value(nk)) * (1.0 / invb) * (1.0 - 0x1p-40);
-        atomicMax(reinterpret_cast<long long*>(cthr + col), __double_as_longlong(t));
-        break;
-      }
+      if (ok == ck && oi == ci) break;
       ck = ok;
       ci = oi;
     }
   }
+  __syncwarp();
+  if (lane == 0) sm.cq_n = 0;
+  __syncwarp();
 }
 
 // SYM exact update, shared by every unrolled step (one copy of the code keeps
@@ -415,8 +443,7 @@ __device__ __noinline__ unsigned exact_update_sym(WarpSmem<R>& sm, int lane, lon
     }
     cm |= (__double2hiint(v) >= tc ? 1u : 0u) << r;
   }
-  if (__any_sync(0xffffffffu, cm != 0))
-    col_update(vals, invn_a, lane, cm, row0, col, invb, excl, nrows, ccand, cthr);
+  if (__any_sync(0xffffffffu, cm != 0)) col_update<R>(sm, vals, lane, cm, row0, col, invb, excl, cthr);
   return upd;
 }
 
@@ -596,6 +623,7 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   // make it resident, retire edge block c-2, start loading chunk c+1 (3-deep
   // rings keep the in-use slots intact)
   auto chunk_turn = [&](int c) {
+    if (SYM && sm.cq_n) col_flush(sm, lane, ccand);
     __syncwarp();
     if (c >= 2 && cx.write_out) {
       flush_block(sm, cx, lane, c - 2);
@@ -629,6 +657,7 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   }
   cp_wait<0>();
   __syncwarp();
+  if (SYM && sm.cq_n) col_flush(sm, lane, ccand);
 #ifdef TSD_COUNT_EXACT
   if (lane == 0) atomicAdd(&g_step_count, (unsigned long long)n);
   if (lane == 0 && cx.first_seg) atomicAdd(&g_step_first, (unsigned long long)n);
@@ -863,6 +892,8 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
   double* Hw = a.hscr + (int64_t)gw * 2048;
   const int bpt = a.bands_per_task;
   const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+  if (lane == 0) sm.cq_n = 0;
+  __syncwarp();
 
   for (int it = 0;; ++it) {
     int task, g, b0, b1;
@@ -889,7 +920,10 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int64_t i = i0 + R * lane + r;
-          if (i < a.nrows && a.flag_a[i] == 1) namin = fmin(namin, 1.0 / a.invn_a[i]);
+          const bool act = i < a.nrows && a.flag_a[i] == 1;
+          const double ia = act ? a.invn_a[i] : 0.0;
+          sm.inva[r][lane] = ia;
+          if (act) namin = fmin(namin, 1.0 / ia);
         }
       }
 #pragma unroll
