@@ -351,25 +351,26 @@ __device__ __forceinline__ void cas128(unsigned long long* p, unsigned long long
 // cm: slots that passed the column threshold. The warp's lexicographic best (max corr, lowest row) is found
 // with three REDUX reductions on the order key and the row.
 template <int R>
-__device__ __noinline__ void col_update(WarpSmem<R>& sm, const double* vals, int lane, unsigned cm, long long row0,
-                                        long long col, double invb, long long excl, double* cthr) {
+__device__ __noinline__ void col_update(WarpSmem<R>& sm, int lane, unsigned cm, int row0, int col, double invb,
+                                        int excl, double* cthr) {
+  // window indices fit 32 bits (the C ABI bounds n), which keeps this rarely
+  // called function inside a few registers (no spills around the sweep)
   unsigned long long bk = 0;  // order key of the lane's best corr (0 = none)
   unsigned brow = 0xffffffffu;
   if (invb > 0.0) {
     for (unsigned mm = cm; mm; mm &= mm - 1) {
       const int r = __ffs(mm) - 1;
-      const long long row = row0 + r;
-      const long long d = col - row;
+      const int d = col - (row0 + r);
       const double ia = sm.inva[r][lane];  // 0 for inactive rows
       if (ia > 0.0 && (d > excl || d < -excl)) {
         // the same rounding as the row side's clamp((cov * invn_b) * invn_a):
         // both rows of a pair see the bitwise-identical correlation, as in the
         // reference (one value updates both, profiles.hpp:289-296)
-        const double c = clamp_corr(vals[r * 32 + lane] * invb * ia);
+        const double c = clamp_corr(sm.slide[r * 32 + lane] * invb * ia);
         const unsigned long long k = order_key(c);
-        if (k > bk || (k == bk && (unsigned)row < brow)) {
+        if (k > bk || (k == bk && (unsigned)(row0 + r) < brow)) {
           bk = k;
-          brow = (unsigned)row;
+          brow = (unsigned)(row0 + r);
         }
       }
     }
@@ -391,7 +392,7 @@ __device__ __noinline__ void col_update(WarpSmem<R>& sm, const double* vals, int
     const int q = sm.cq_n;
     sm.cq_key[q] = wk;
     sm.cq_row[q] = wrow;
-    sm.cq_col[q] = (int)col;
+    sm.cq_col[q] = col;
     sm.cq_n = q + 1;
   }
 }
@@ -426,24 +427,22 @@ __device__ __noinline__ void col_flush(WarpSmem<R>& sm, int lane, unsigned long 
 // sweep_block; column side via col_update. Returns the lane's mask of slots
 // whose best changed (the caller refreshes their thresholds).
 template <int R>
-__device__ __noinline__ unsigned exact_update_sym(WarpSmem<R>& sm, int lane, long long col, double invb, int tc,
-                                                  long long row0, long long excl, const double* __restrict__ invn_a,
-                                                  long long nrows, unsigned long long* ccand, double* cthr) {
-  const double* vals = sm.slide;
+__device__ __noinline__ unsigned exact_update_sym(WarpSmem<R>& sm, int lane, int col, double invb, int tc, int row0,
+                                                  int excl, double* cthr) {
   unsigned upd = 0, cm = 0;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const double v = vals[r * 32 + lane];
+    const double v = sm.slide[r * 32 + lane];
     const double K = v * invb;
-    const long long d = row0 + r - col;
+    const int d = row0 + r - col;
     if (K > sm.bK[r][lane] && (d > excl || d < -excl)) {  // profiles.hpp:70-77, :281-284
       sm.bK[r][lane] = K;
-      sm.bj[r][lane] = (int)col;
+      sm.bj[r][lane] = col;
       upd |= 1u << r;
     }
     cm |= (__double2hiint(v) >= tc ? 1u : 0u) << r;
   }
-  if (__any_sync(0xffffffffu, cm != 0)) col_update<R>(sm, vals, lane, cm, row0, col, invb, excl, cthr);
+  if (__any_sync(0xffffffffu, cm != 0)) col_update<R>(sm, lane, cm, row0, col, invb, excl, cthr);
   return upd;
 }
 
@@ -567,7 +566,7 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
         __syncwarp();
         const int tc = __double2hiint(sm.cring[ebase + u] * cx.namin);  // this column's own threshold
         const unsigned upd =
-            exact_update_sym<R>(sm, lane, col, invb, tc, cx.row0, cx.excl, invn_a, nrows, ccand, cthr);
+            exact_update_sym<R>(sm, lane, col, invb, tc, (int)cx.row0, (int)cx.excl, cthr);
         __syncwarp();
         if (upd) {
 #pragma unroll
