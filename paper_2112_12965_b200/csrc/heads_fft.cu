@@ -227,7 +227,7 @@ struct HeadsArgs {
   const double2* tw;
   const double* ebt;  // sum of btil per segment
   const SegDev* segs;
-  const double4* col;     // FP64 packed column data (.z = invn_b), read for the seeds
+  const double* invn_b;   // column invn (seeds: K = head * invn_b, as the sweeps compute it)
   const uint8_t* flag_a;  // row flags (bit0 valid, bit1 flat)
   int nseg, npairs, m, Q;
   long long excl;  // self-join exclusion half-width (-1: AB join)
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
     const bool two = s1 < a.nseg;
     const int64_t c0 = a.segs[s0].col0, c1 = two ? a.segs[s1].col0 : c0;
     const double e0 = a.ebt[s0], e1 = two ? a.ebt[s1] : 0.0;
-    const double k0 = a.seed ? a.col[c0].z : 0.0, k1 = (two && a.seed) ? a.col[c1].z : 0.0;
+    const double k0 = a.seed ? a.invn_b[c0] : 0.0, k1 = (two && a.seed) ? a.invn_b[c1] : 0.0;
     asm volatile("cp.async.wait_group 0;\n" ::);
     double2 v[16];
 #pragma unroll
@@ -341,7 +341,8 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
 int heads_fft_supported(int m) { return m >= 1 && m <= FFT_N - 512 + 1; }
 
 int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrows, const double* d_mua,
-                      const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
+                      const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double* d_invn_b,
+                      const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
                       unsigned long long* d_seed, long long excl, int sym, Arena& arena, cudaStream_t st,
                       int* launches, Error* err) {
   const int npairs = (nseg + 1) / 2;
@@ -368,7 +369,7 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
   a.tw = d_tw;
   a.ebt = d_ebt;
   a.segs = d_segs;
-  a.col = d_col;
+  a.invn_b = d_invn_b;
   a.flag_a = d_flag_a;
   a.nseg = nseg;
   a.npairs = npairs;

@@ -932,7 +932,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
         sm.bK[r][lane] = f == 1 ? -kInf : kInf;  // valid non-flat rows take part; +inf never passes
         sm.bj[r][lane] = -1;
       }
-      if (!F32 && a.seed) {
+      if (a.seed) {
         // Seed each row's best with its precomputed lower bound: one ulp below
         // the best column-0 candidate over ALL segments (heads_fft.cu). The
         // cell achieving it is visited by exactly one group and recorded by
@@ -947,7 +947,10 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           const unsigned long long key = sm.bK[r][lane] == -kInf ? a.seed[i] : 0ull;  // -inf: valid row
           if (key != 0ull) {
             const unsigned long long bits = (key >> 63) ? (key & 0x7fffffffffffffffull) : ~key;
-            sm.bK[r][lane] = nextafter(__longlong_as_double((long long)bits), -kInf);
+            const double kb = nextafter(__longlong_as_double((long long)bits), -kInf);
+            // FP32 sweep: its value of the seed cell differs by FP32 rounding
+            // (~6e-8 relative); a 1e-6 margin keeps the seed strictly below it
+            sm.bK[r][lane] = F32 ? (kb > 0.0 ? kb * (1.0 - 1e-6) : kb * (1.0 + 1e-6)) : kb;
           }
         }
       }
@@ -1616,12 +1619,13 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     const size_t hbytes = sizeof(double) * (size_t)nseg * (size_t)hstride;
     if (want && cudaMemGetInfo(&fr, &tot) == cudaSuccess && hbytes < fr / 2) {
       d_heads = (double*)arena.get(hbytes);
-      d_seed = F32 ? nullptr : (unsigned long long*)arena.get(sizeof(unsigned long long) * nrows);
-      if (d_heads && (F32 || d_seed)) {
+      d_seed = (unsigned long long*)arena.get(sizeof(unsigned long long) * nrows);
+      if (d_heads && d_seed) {
         if (in.ev[0]) CUDA_TRY(cudaEventRecord(in.ev[0], st));
         in.heads_used = true;
         const int rc = compute_heads_fft(in.xa, in.na, nrows, hstride, in.rows.mu, in.rows.flag, d_btil, d_ebt,
-                                         d_col, d_segs, nseg, m, d_heads, hstride, d_seed, SELF ? in.excl : -1,
+                                         in.cols.invn, d_segs, nseg, m, d_heads, hstride, d_seed,
+                                         SELF ? in.excl : -1,
                                          SYM ? 1 : 0, arena, st, &nl, err);
         if (rc != kOk) return rc;
         if (in.ev[1]) CUDA_TRY(cudaEventRecord(in.ev[1], st));

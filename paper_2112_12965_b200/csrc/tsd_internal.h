@@ -125,7 +125,8 @@ int heads_fft_supported(int m);
 // none; excl >= 0: self-join, heads inside the exclusion zone skipped); one
 // ulp below it is a strict lower bound the join starts from (k_join).
 int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrows, const double* d_mua,
-                      const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double4* d_col, const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
+                      const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double* d_invn_b,
+                      const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
                       unsigned long long* d_seed, long long excl, int sym, Arena& arena, cudaStream_t st,
                       int* launches, Error* err);
 
