@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
   for (int p = p0; p < p1; ++p) {
     const int s0 = 2 * p, s1 = 2 * p + 1;
     const bool two = s1 < a.nseg;
-    const int64_t c0 = a.segs[s0].col0, c1 = two ? a.segs[s1].col0 : c0;
+    const int64_t c0 = a.seed ? a.segs[s0].col0 : 0, c1 = (two && a.seed) ? a.segs[s1].col0 : c0;
     const double e0 = a.ebt[s0], e1 = two ? a.ebt[s1] : 0.0;
     const double k0 = a.seed ? a.invn_b[c0] : 0.0, k1 = (two && a.seed) ? a.invn_b[c1] : 0.0;
     asm volatile("cp.async.wait_group 0;\n" ::);

@@ -91,6 +91,8 @@ struct JoinArgs {
   const double* heads;  // precomputed final heads [seg][hstride] (heads_fft.cu), or null
   int64_t hstride;
   const unsigned long long* seed;  // per-row order key of the best head candidate (heads_fft.cu), or null
+  const double* tedge;  // top edges by FFT: tedge[r * tstride + c] = cov(top row of band range r, column c), or null
+  int64_t tstride;
   double* out_c;  // [ngroups][nrows]
   int64_t* out_j;
   // symmetric self-join (SYM kernels): task queue and the column side
@@ -995,7 +997,20 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
         cx.first_seg = (s == s_beg);
         cx.cthr = SYM ? a.cthr + sg.col0 : nullptr;
         cx.namin = namin;
-        if (b == b0 && sg.ncol >= 2) {
+        if (b == b0 && sg.ncol >= 2 && a.tedge) {
+          // top edge precomputed by FFT correlation: E[q - delta] = cov(re, col0 + q)
+          const int delta = i0 >= 1 ? 0 : 1;
+          const double* te = a.tedge + (int64_t)(b0 / bpt) * a.tstride + sg.col0;
+          for (int q = delta + lane; q < sg.ncol - 1 + delta; q += 32) {
+            const double v = te[q] * (F32 ? a.scale[sg.col0 + q - delta] : 1.0);
+            if constexpr (F32)
+              reinterpret_cast<float*>(cx.E)[q - delta] = (float)v;
+            else
+              cx.E[q - delta] = v;
+          }
+          __threadfence_block();
+          __syncwarp();
+        } else if (b == b0 && sg.ncol >= 2) {
           // top edge of the task: E[j] = cov(re, j + delta), j = 0 .. ncol-2
           // (row 0 has df = dg = 0, so E[j] = cov(0, j+1) feeds it exactly)
           const int64_t re = i0 >= 1 ? i0 - 1 : 0;
@@ -1137,6 +1152,31 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
       __syncwarp();
     }
   }
+}
+
+// centred top window of each band range (row re = first row - 1, or 0 for
+// the first range): w[r][k] = x[re + k] - mu[re], e[r] = sum_k w[r][k]
+__global__ void k_topwin(const double* __restrict__ x, const double* __restrict__ mu, int nbr, int rows_per_range,
+                         int m, double* __restrict__ w, double* __restrict__ e) {
+  const int r = blockIdx.x;
+  if (r >= nbr) return;
+  const int64_t i0 = (int64_t)r * rows_per_range;
+  const int64_t re = i0 >= 1 ? i0 - 1 : 0;
+  const double c = mu[re];
+  double s = 0.0;
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
+    const double v = x[re + k] - c;
+    w[(int64_t)r * m + k] = v;
+    s += v;
+  }
+  __shared__ double sh[128];
+  sh[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 64; o > 0; o >>= 1) {
+    if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) e[r] = sh[0];
 }
 
 // merge of per-group partials (lexicographic, group order = column order)
@@ -1469,7 +1509,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
         smax = std::max<int64_t>(smax, gs[q + 1] - gs[q]);
       }
       const double band = (double)H * (3.0 * cmax + (double)smax * (m + 64)) + 24.0 * cmax;
-      const double top = (double)cmax * m;
+      // top edge of a task: a copy from the FFT table, else an m-term dot per column
+      const double top = (double)cmax * (heads_fft_supported(m) ? 16.0 : (double)m);
       const int bmax = std::min(nbands, F32 ? 4096 / H : 4096);
       for (int b = 1; b <= bmax; ++b) {
         const int64_t nt = (int64_t)((nbands + b - 1) / b) * g;
@@ -1632,6 +1673,32 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       }
     }
   }
+  // top edges by FFT: one row of the table per band range, all columns
+  double* d_te = nullptr;
+  int64_t tstride = 0;
+  {
+    const char* e = getenv("TSD_FFT_TOP");
+    const int nbr_t = (nbands + bpt - 1) / bpt;
+    tstride = (in.cols.nwin + 1) & ~int64_t(1);
+    size_t fr = 0, tot = 0;
+    const size_t tbytes = sizeof(double) * (size_t)nbr_t * (size_t)tstride;
+    if ((e ? atoi(e) != 0 : true) && heads_fft_supported(m) && nbr_t >= 2 &&
+        cudaMemGetInfo(&fr, &tot) == cudaSuccess && tbytes < fr / 4) {
+      double* d_tw = (double*)arena.get(sizeof(double) * (size_t)nbr_t * m);
+      double* d_tew = (double*)arena.get(sizeof(double) * nbr_t);
+      d_te = (double*)arena.get(tbytes);
+      if (d_tw && d_tew && d_te) {
+        k_topwin<<<nbr_t, 128, 0, st>>>(in.xa, in.rows.mu, nbr_t, bpt * H, m, d_tw, d_tew);
+        ++nl;
+        const int rc = compute_heads_fft(in.xb, in.nb, in.cols.nwin, in.cols.nwin, in.cols.mu, in.cols.flag, d_tw,
+                                         d_tew, in.cols.invn, d_segs, nbr_t, m, d_te, tstride, nullptr, -1, 0, arena,
+                                         st, &nl, err);
+        if (rc != kOk) return rc;
+      } else {
+        d_te = nullptr;
+      }
+    }
+  }
   JoinArgs a;
   a.xa = in.xa;
   a.na = in.na;
@@ -1666,6 +1733,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   a.heads = d_heads;
   a.hstride = hstride;
   a.seed = d_heads ? d_seed : nullptr;
+  a.tedge = d_te;
+  a.tstride = tstride;
   a.tasks = d_tasks;
   a.task_next = d_tnext;
   a.ccand = d_ccand;
