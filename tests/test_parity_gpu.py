@@ -243,6 +243,35 @@ def test_fft_heads_vs_direct_heads_and_oracle(monkeypatch, m, nseg, L):
     check_profile(P.values, P.indices, rv, ri, m, dd, label=f"fft vs oracle m={m}")
 
 
+@pytest.mark.parametrize("kind", ["dict", "self"])
+def test_fft_top_edges_vs_direct_top_edges(monkeypatch, kind):
+    """task top edges from the FFT table (heads_fft.cu with the roles swapped,
+    the default) against the in-kernel sliding dot (TSD_FFT_TOP=0) and the
+    oracle; many band ranges so most tasks start below row 0"""
+    m = 200
+    if kind == "dict":
+        q = synth.walk(71, 300000)
+        segs = list(synth.walks(72, 24, 1500))
+        starts = [3000 * s for s in range(24)]
+        D = _dict(segs, starts, m)
+        run = lambda: tsd.join_dictionary(q, D, m)
+    else:
+        q = synth.walk(73, 120000)
+        run = lambda: tsd.self_join(q, m)
+    monkeypatch.setenv("TSD_FFT_TOP", "1")
+    P = run()
+    monkeypatch.setenv("TSD_FFT_TOP", "0")
+    Pd = run()
+    dist = dict_dist(q, segs, starts, m) if kind == "dict" else ab_dist(q, q, m)
+    check_profile(P.values, P.indices, Pd.values, Pd.indices, m, dist, label=f"fft top vs direct ({kind})")
+    rng = np.random.default_rng(7)
+    for i in rng.choice(P.values.size, 12, replace=False):
+        if kind == "dict":
+            rv, ri = O.dict_join(q[i:i + m], segs, starts, m)
+            check_profile(P.values[i:i + 1], P.indices[i:i + 1], rv, ri, m, dict_dist(q[i:i + m], segs, starts, m),
+                          label=f"fft top row {i}")
+
+
 @pytest.mark.parametrize("precision", ["fp64", "fp32"])
 def test_adversarial_dictionary_thresholds_and_seeds(precision):
     """Edge cases of the row test and the head seeds, against the oracle:
