@@ -90,7 +90,9 @@ struct JoinArgs {
   int dmma_heads; // heads on the FP64 tensor cores (else register-blocked sliding dot)
   const double* heads;  // precomputed final heads [seg][hstride] (heads_fft.cu), or null
   int64_t hstride;
-  const unsigned long long* seed;  // per-row order key of the best head candidate (heads_fft.cu), or null
+  // per-row order key of the best known candidate, or null: seeded by the
+  // heads (heads_fft.cu) and raised by every finished band (non-SYM)
+  unsigned long long* seed;
   const double* tedge;  // top edges by FFT: tedge[r * tstride + c] = cov(top row of band range r, column c), or null
   int64_t tstride;
   double* out_c;  // [ngroups][nrows]
@@ -123,7 +125,8 @@ struct __align__(16) WarpSmem {
 };
 
 #ifdef TSD_COUNT_EXACT
-__device__ unsigned long long g_exact_count, g_step_count, g_exact_first, g_step_first, g_col_count, g_cas_count;
+__device__ unsigned long long g_exact_count, g_step_count, g_exact_first, g_step_first, g_col_count, g_cas_count,
+    g_true_steps, g_true_slots;
 #endif
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -579,6 +582,9 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
             }
         }
       } else {
+#ifdef TSD_COUNT_EXACT
+      int nupd = 0;
+#endif
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const double K = S.P[(r + ph) & (R - 1)] * invb;
@@ -593,7 +599,18 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
           S.bKp[r] = kplus(K);
           S.thr[r] = __double2hiint(S.bKp[r] * nmin);
         }
+#ifdef TSD_COUNT_EXACT
+        nupd += ok;
+#endif
       }
+#ifdef TSD_COUNT_EXACT
+      {
+        const unsigned any = __ballot_sync(0xffffffffu, nupd > 0);
+        for (int o = 16; o; o >>= 1) nupd += __shfl_xor_sync(0xffffffffu, nupd, o);
+        if (lane == 0 && any) atomicAdd(&g_true_steps, 1ull);
+        if (lane == 0) atomicAdd(&g_true_slots, (unsigned long long)nupd);
+      }
+#endif
       }
     }
   }
@@ -888,7 +905,6 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   WarpSmem<R>& sm = smem[wl];
   const int gw = blockIdx.x * WARPS + wl;
-  const int nw = gridDim.x * WARPS;
   double* Ew = a.edges + (int64_t)gw * a.ecap;
   double* Hw = a.hscr + (int64_t)gw * 2048;
   const int bpt = a.bands_per_task;
@@ -907,10 +923,15 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
       b1 = t4.y;
       g = t4.z;
     } else {
-      task = gw + it * nw;
+      // dynamic queue, group-major: the groups of one band range run in
+      // different waves, so each starts from the bests published by the
+      // earlier ones (fewer record updates)
+      if (lane == 0) task = atomicAdd(a.task_next, 1);
+      task = __shfl_sync(0xffffffffu, task, 0);
       if (task >= a.ntasks) break;
-      g = task % a.ngroups;
-      b0 = (task / a.ngroups) * bpt;
+      const int nbr = (a.nbands + bpt - 1) / bpt;
+      g = task / nbr;
+      b0 = (task - g * nbr) * bpt;
       b1 = min(a.nbands, b0 + bpt);
     }
     const int s_beg = a.group_seg[g], s_end = a.group_seg[g + 1];
@@ -946,7 +967,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int64_t i = i0 + R * lane + r;
-          const unsigned long long key = sm.bK[r][lane] == -kInf ? a.seed[i] : 0ull;  // -inf: valid row
+          const unsigned long long key = sm.bK[r][lane] == -kInf ? __ldcg(a.seed + i) : 0ull;  // -inf: valid row
           if (key != 0ull) {
             const unsigned long long bits = (key >> 63) ? (key & 0x7fffffffffffffffull) : ~key;
             const double kb = nextafter(__longlong_as_double((long long)bits), -kInf);
@@ -1147,6 +1168,10 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           const int j = sm.bj[r][lane];
           oc[i] = j >= 0 ? clamp_corr(sm.bK[r][lane] * a.invn_a[i]) : -2.0;
           oj[i] = j;
+          // publish the band's best: later tasks on these rows (other groups)
+          // start from it. It is exactly the K this group's sweep computed for
+          // the recorded cell, so the seed argument above holds for it too.
+          if (!SYM && j >= 0 && a.seed) atomicMax(a.seed + i, order_key(sm.bK[r][lane]));
         }
       }
       __syncwarp();
@@ -1480,7 +1505,11 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   // segments). Cost model in FP64-op units per warp: a band sweeps its
   // group's cells (3 ops) plus one m-term head per row per segment; the first
   // band of a task also computes the group's top edge (m terms per column).
-  // Pick (G, bpt) minimising waves * task cost; G > 1 costs a merge pass.
+  // Tasks are handed out dynamically: several waves cost the total over all
+  // warps plus half a task (the tail); a single wave costs one task over the
+  // fraction of warps it fills (the SMs are issue-bound, and its slowest task
+  // sets the end). G > 1 costs a merge pass. Calibrated on C4 and C2:
+  // profiles/README.md.
   int64_t total_cols = 0;
   for (const auto& s : segs) total_cols += s.ncol;
   auto split = [&](int G, std::vector<int>& gs) {
@@ -1508,22 +1537,30 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
         cmax = std::max(cmax, c);
         smax = std::max<int64_t>(smax, gs[q + 1] - gs[q]);
       }
-      const double band = (double)H * (3.0 * cmax + (double)smax * (m + 64)) + 24.0 * cmax;
-      // top edge of a task: a copy from the FFT table, else an m-term dot per column
-      const double top = (double)cmax * (heads_fft_supported(m) ? 16.0 : (double)m);
+      // per row and segment: an FFT head (a load) or an m-term direct head
+      const bool fft = heads_fft_supported(m);
+      const double band = (double)H * (3.0 * cmax + (double)smax * (fft && nseg >= 2 ? 16.0 : m + 64.0)) + 24.0 * cmax;
+      // top edge of a task: its row of the FFT table (~16 sweep cells of
+      // transform work per column), else an m-term dot per column
+      const double top = (double)cmax * (fft ? 50.0 : (double)m);
       const int bmax = std::min(nbands, F32 ? 4096 / H : 4096);
       for (int b = 1; b <= bmax; ++b) {
         const int64_t nt = (int64_t)((nbands + b - 1) / b) * g;
-        const int64_t waves = (nt + nwarps - 1) / nwarps;
-        const double cost = waves * (b * band + top) + (g > 1 ? 2e3 * (double)nrows * g / nwarps : 0.0);
+        const double tc = b * band + top;
+        const double run = nt <= nwarps ? tc * nwarps / (double)nt : (double)nt * tc / nwarps + 0.5 * tc;
+        const double cost = run + (g > 1 ? 2e3 * (double)nrows * g / nwarps : 0.0);
         if (cost < best * 0.999) {
           best = cost;
           G = g;
           bpt = b;
         }
-        if (waves == 1) break;  // larger b only adds work per task
+        if (nt <= nwarps) break;  // larger b only adds work per task
       }
     }
+  }
+  if (!SYM && getenv("TSD_FORCE_G") && getenv("TSD_FORCE_BPT")) {  // development override
+    G = std::max(1, std::min(nseg, atoi(getenv("TSD_FORCE_G"))));
+    bpt = std::max(1, atoi(getenv("TSD_FORCE_BPT")));
   }
   // SYM: one group per piece; bands sweep only their triangle part, so task
   // sizes differ -- choose bpt by an LPT (longest first onto the least-loaded
@@ -1614,9 +1651,14 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   int* d_tnext = nullptr;
   unsigned long long* d_ccand = nullptr;
   double* d_cthr = nullptr;
+  d_tnext = (int*)arena.get(sizeof(int));
+  if (!d_tnext) {
+    if (err) *err = Error{kCudaError, "device allocation failed for the join"};
+    return kCudaError;
+  }
+  CUDA_TRY(cudaMemsetAsync(d_tnext, 0, sizeof(int), st));
   if (SYM) {
     d_tasks = (int4*)arena.get(sizeof(int4) * std::max<size_t>(1, sym_tasks.size()));
-    d_tnext = (int*)arena.get(sizeof(int));
     d_ccand = (unsigned long long*)arena.get(sizeof(unsigned long long) * 2 * SYM_NC * (in.cols.nwin + 64));
     d_cthr = (double*)arena.get(sizeof(double) * (in.cols.nwin + 64));
     if (!d_tasks || !d_tnext || !d_ccand || !d_cthr) {
@@ -1626,7 +1668,6 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     if (!sym_tasks.empty())
       CUDA_TRY(cudaMemcpyAsync(d_tasks, sym_tasks.data(), sizeof(int4) * sym_tasks.size(), cudaMemcpyHostToDevice,
                                st));
-    CUDA_TRY(cudaMemsetAsync(d_tnext, 0, sizeof(int), st));
     // (band range, group) pairs without columns are never queued: their
     // partial rows must read "no candidate" in the merge
     CUDA_TRY(cudaMemsetAsync(d_pj, 0xff, sizeof(int64_t) * nrows * G, st));
@@ -1732,7 +1773,12 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   }
   a.heads = d_heads;
   a.hstride = hstride;
-  a.seed = d_heads ? d_seed : nullptr;
+  if (!SYM && !d_heads) {
+    // no head seeds: the array still carries the bests finished bands publish
+    d_seed = (unsigned long long*)arena.get(sizeof(unsigned long long) * nrows);
+    if (d_seed) CUDA_TRY(cudaMemsetAsync(d_seed, 0, sizeof(unsigned long long) * nrows, st));
+  }
+  a.seed = (d_heads || !SYM) ? d_seed : nullptr;
   a.tedge = d_te;
   a.tstride = tstride;
   a.tasks = d_tasks;
@@ -1756,6 +1802,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   cudaMemcpyToSymbol(g_step_first, &zero, 8);
   cudaMemcpyToSymbol(g_col_count, &zero, 8);
   cudaMemcpyToSymbol(g_cas_count, &zero, 8);
+  cudaMemcpyToSymbol(g_true_steps, &zero, 8);
+  cudaMemcpyToSymbol(g_true_slots, &zero, 8);
 #endif
   if (in.ev[2]) CUDA_TRY(cudaEventRecord(in.ev[2], st));
   kern<<<grid, 32 * WARPS, smem_bytes, st>>>(a);
@@ -1778,6 +1826,11 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     cudaMemcpyFromSymbol(&ca, g_cas_count, 8);
     fprintf(stderr, "[tsd] column-side updates %llu (%.2f%% of warp-steps), with a candidate %llu\n", cc,
             100.0 * cc / (cs ? cs : 1), ca);
+    unsigned long long ts = 0, tsl = 0;
+    cudaMemcpyFromSymbol(&ts, g_true_steps, 8);
+    cudaMemcpyFromSymbol(&tsl, g_true_slots, 8);
+    fprintf(stderr, "[tsd] warp-steps with a true update %.2f%%, updated slots per warp-step %.4f\n",
+            100.0 * ts / (cs ? cs : 1), (double)tsl / (cs ? cs : 1));
   }
 #endif
   if (SYM) {
