@@ -6,6 +6,7 @@
 // re-entrant). There is no CPU fallback: when no usable CUDA device exists
 // every entry point fails with TSD_CUDA_ERROR.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -231,7 +232,17 @@ int plan_join_dev(tsd_dict_plan* p, const double* d_q, const size_t* q_len, size
   return kOk;
 }
 
+// TSD_VERBOSE: host time since t0 with the stream drained
+static void verbose_phase(const char* what, cudaStream_t st, std::chrono::steady_clock::time_point t0) {
+  static const bool on = getenv("TSD_VERBOSE") != nullptr;
+  if (!on) return;
+  cudaStreamSynchronize(st);
+  fprintf(stderr, "[tsd] %s at %.2f ms\n", what,
+          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+}
+
 int plan_join_host(tsd_dict_plan* p, const double* q, const size_t* q_len, size_t nser, double* val, int64_t* idx) {
+  const auto t0 = std::chrono::steady_clock::now();
   int64_t N = 0, outn = 0;
   for (size_t k = 0; k < nser; ++k) {
     if ((size_t)p->m > q_len[k]) return fail(kWindowTooLarge, "window length exceeds series length");
@@ -247,10 +258,13 @@ int plan_join_host(tsd_dict_plan* p, const double* q, const size_t* q_len, size_
   if (!d_q || !d_val || !d_idx) return fail(kCudaError, "device allocation failed for the query");
   cudaStream_t st = p->s.st;
   CK(cudaMemcpyAsync(d_q, q, sizeof(double) * N, cudaMemcpyHostToDevice, st));
+  verbose_phase("query upload", st, t0);
   if (int rc = plan_join_dev(p, d_q, q_len, nser, d_val, d_idx, st)) return rc;
+  verbose_phase("join", st, t0);
   CK(cudaMemcpyAsync(val, d_val, sizeof(double) * outn, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(idx, d_idx, sizeof(int64_t) * outn, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  verbose_phase("profile download", st, t0);
   return kOk;
 }
 
@@ -305,6 +319,14 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
   tc.arena.reset();
   cudaStream_t st = tc.s.st;
   const bool self = (b == nullptr);
+  const bool verbose = getenv("TSD_VERBOSE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {  // TSD_VERBOSE: host time since entry, stream drained
+    if (!verbose) return;
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[tsd] %s at %.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  };
   double* d_a = (double*)tc.arena.get(sizeof(double) * (na + 64));
   double* d_b = self ? d_a : (double*)tc.arena.get(sizeof(double) * (nb + 64));
   if (self) nb = na;
@@ -329,6 +351,7 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
     TRY(compute_windows(d_b, (int64_t)nb, (int)m, gb, 1, in.cols, tc.arena, st, &bad, &er));
     if (bad >= 0) return fail(kNonFiniteInput, "series contains a non-finite sample");
   }
+  phase("inputs + window statistics");
   in.xa = d_a;
   in.na = (int64_t)na;
   in.xb = d_b;
@@ -351,7 +374,16 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
     CK(cudaMemcpyAsync(d_bj, idx, sizeof(int64_t) * nrows, cudaMemcpyHostToDevice, st));
   } else {
     TRY(run_join(in, d_bc, d_bj, tc.arena, st, &er, &launches));
+    if (self && getenv("TSD_PERFECT_SEED")) {  // development probe: rerun seeded from the final bests
+      double* d_lb = (double*)tc.arena.get(sizeof(double) * nrows);
+      if (!d_lb) return fail(kCudaError, "device allocation failed");
+      CK(cudaMemcpyAsync(d_lb, d_bc, sizeof(double) * nrows, cudaMemcpyDeviceToDevice, st));
+      in.seed_corr = d_lb;
+      in.seed_margin = atof(getenv("TSD_PERFECT_SEED"));
+      TRY(run_join(in, d_bc, d_bj, tc.arena, st, &er, &launches));
+    }
   }
+  phase("join");
   if (stage == 1) {
     CK(cudaMemcpyAsync(val, d_bc, sizeof(double) * nrows, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(idx, d_bj, sizeof(int64_t) * nrows, cudaMemcpyDeviceToHost, st));
@@ -363,6 +395,7 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
   CK(cudaMemcpyAsync(val, d_val, sizeof(double) * nrows, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(idx, d_idx, sizeof(int64_t) * nrows, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  phase("epilogue + outputs");
   return kOk;
 }
 

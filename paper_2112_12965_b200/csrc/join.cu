@@ -31,6 +31,7 @@
 //     Flat rows (invn_a == 0) are resolved in the epilogue from the flat
 //     column table (profiles.hpp:332-336 gives them c in {0, 1}).
 #include <algorithm>
+#include <chrono>
 #include <queue>
 #include <cfloat>
 #include <climits>
@@ -527,7 +528,11 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
     const int ph = (R - u) & (R - 1);  // physical register of slot 0 at this step
     if (u % TB == 0) {  // threshold block of TB columns (nmin prefetched with its first column)
       nmin = (FIRST && u == 0) ? ccur[0].w : S.nx.nmin;
+#ifdef TSD_ABL_NOCOLFOLD
+      if (false) {
+#else
       if (SYM) {  // column side folded in: the block's weakest column threshold
+#endif
         double cmin = sm.cring[ebase + u];
 #pragma unroll
         for (int t = 1; t < TB; ++t) cmin = fmin(cmin, sm.cring[ebase + u + t]);
@@ -552,7 +557,9 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
       prefetch((u + 1) % TB == 0, u + 1 < R ? ccur + u + 1 : cnext, &sm.ering[ebase + u],
                S.P[(ph + R - 1) & (R - 1)], S.nx);
 #ifdef TSD_ABL_NOEXACT
-    if (vote_any8(S.P, ph, S.thr) && cx.ncol < 0) [[unlikely]] {
+    unsigned opaque0;  // 0, invisible to the compiler: the test stays, the exact update never runs
+    asm volatile("mov.u32 %0, 0;" : "=r"(opaque0));
+    if (vote_any8(S.P, ph, S.thr) && opaque0) [[unlikely]] {
 #else
     if (vote_any8(S.P, ph, S.thr)) [[unlikely]] {
 #endif
@@ -1437,6 +1444,20 @@ __global__ void k_merge_sym(const double* __restrict__ pc, const int64_t* __rest
   oj[i] = bj;
 }
 
+// Row seeds from external lower bounds lb[i] (corr units, <= -2: none): the
+// order key of (lb - margin) / invn_a in the sweep's K units (k_join)
+__global__ void k_seed_fold(unsigned long long* __restrict__ seed, const double* __restrict__ lb,
+                            const double* __restrict__ invn, const uint8_t* __restrict__ flag, int64_t n,
+                            double margin) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double iv = invn[i];
+  const double c = lb[i] - margin;
+  if (flag[i] != 1 || !(iv > 0.0) || !(c > -1.0)) return;
+  const unsigned long long key = order_key(c / iv);
+  if (key > seed[i]) seed[i] = key;
+}
+
 // SYM: column side initial state from the row seeds (a lower bound of each
 // row's final best, never reported: index "none" = ~0)
 __global__ void k_sym_init(const unsigned long long* __restrict__ seed, const double* __restrict__ invn,
@@ -1470,6 +1491,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   // several segment groups and tall tasks (few top edges). Column numbering,
   // masks and the epilogue's source mapping are unchanged; each piece starts
   // from its own head (cov at its first column), exactly as a segment does.
+  const auto t_host0 = std::chrono::steady_clock::now();
   std::vector<SegDev> vsegs;
   {
     int64_t tot = 0;
@@ -1566,7 +1588,28 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   // sizes differ -- choose bpt by an LPT (longest first onto the least-loaded
   // warp) makespan estimate and hand tasks out dynamically in that order
   std::vector<int4> sym_tasks;
+  // the LPT plan depends only on the shape: repeated calls of one shape (a
+  // learning loop, a benchmark) reuse it
+  struct SymPlan {
+    std::vector<int64_t> key;
+    std::vector<int4> tasks;
+    int bpt;
+  };
+  static thread_local SymPlan sym_cache;
+  std::vector<int64_t> sym_key;
   if constexpr (SYM) {
+    sym_key = {nrows, (int64_t)nseg, in.excl, (int64_t)m, (int64_t)H, (int64_t)nwarps, (int64_t)in.shard,
+               (int64_t)in.nshards};
+    for (const auto& sg : segs) {
+      sym_key.push_back(sg.col0);
+      sym_key.push_back(sg.ncol);
+    }
+  }
+  if (SYM && sym_cache.key == sym_key) {
+    G = nseg;
+    sym_tasks = sym_cache.tasks;
+    bpt = sym_cache.bpt;
+  } else if constexpr (SYM) {
     G = nseg;
     auto qoff = [&](int b, int sgi) -> int64_t {  // first swept local column (kernel: q)
       const int64_t d = (int64_t)b * H + in.excl + 1 - segs[sgi].col0;
@@ -1575,13 +1618,30 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     double best = 1e300;
     int bbest = 1;
     std::vector<std::pair<double, int4>> cand;
-    for (int bp = 1; bp <= std::min(nbands, 1024); bp *= 2) {
+    // per piece: prefix sums over bands of the swept cells (cost units), so a
+    // candidate task's cost is O(1)
+    std::vector<double> pre((size_t)G * (nbands + 1));
+    for (int g = 0; g < G; ++g) {
+      double* P = pre.data() + (size_t)g * (nbands + 1);
+      P[0] = 0.0;
+      for (int b = 0; b < nbands; ++b) P[b + 1] = P[b] + (double)H * 2.5 * (double)(segs[g].ncol - qoff(b, g));
+    }
+    const int bpmax = std::min(nbands, 1024);
+    for (int bp = 1; bp <= bpmax; bp *= 2) {
+      // very fine splits only add per-task overhead (top edge, head) once
+      // there are many tasks per warp; skip them while a coarser one remains
+      if (bp * 2 <= bpmax) {
+        int64_t cnt = 0;
+        for (int g = 0; g < G; ++g)
+          for (int b0 = 0; b0 < nbands; b0 += bp) cnt += qoff(b0, g) < segs[g].ncol;
+        if (cnt > 32 * (int64_t)nwarps) continue;
+      }
       cand.clear();
       for (int b0 = 0; b0 < nbands; b0 += bp) {
         const int b1 = std::min(nbands, b0 + bp);
         for (int g = 0; g < G; ++g) {
-          double c = 0.0;
-          for (int b = b0; b < b1; ++b) c += (double)H * 2.5 * (double)(segs[g].ncol - qoff(b, g));
+          const double* P = pre.data() + (size_t)g * (nbands + 1);
+          double c = P[b1] - P[b0];
           if (c <= 0.0) continue;
           c += (double)(segs[g].ncol - qoff(b0, g)) * m + (double)H * m;  // top edge + head
           cand.push_back({c, make_int4(b0, b1, g, 0)});
@@ -1608,6 +1668,9 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       }
     }
     bpt = bbest;
+    sym_cache.key = sym_key;
+    sym_cache.tasks = sym_tasks;
+    sym_cache.bpt = bpt;
   }
   std::vector<int> group_seg;
   if (SYM) {
@@ -1632,8 +1695,10 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   const int grid = std::max(1, std::min(nsm * occ, (ntasks + WARPS - 1) / WARPS));
   const int used_warps = grid * WARPS;
   if (getenv("TSD_VERBOSE"))
-    fprintf(stderr, "[tsd] join R=%d rows=%lld bands=%d cols=%lld segs=%d -> G=%d bpt=%d tasks=%d warps=%d occ=%d\n", R,
-            (long long)nrows, nbands, (long long)total_cols, nseg, G, bpt, ntasks, used_warps, occ);
+    fprintf(stderr,
+            "[tsd] join R=%d rows=%lld bands=%d cols=%lld segs=%d -> G=%d bpt=%d tasks=%d warps=%d occ=%d (plan %.2f ms)\n",
+            R, (long long)nrows, nbands, (long long)total_cols, nseg, G, bpt, ntasks, used_warps, occ,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count());
 
   SegDev* d_segs = (SegDev*)arena.get(sizeof(SegDev) * nseg);
   int* d_eoff = (int*)arena.get(sizeof(int) * nseg);
@@ -1778,7 +1843,23 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     d_seed = (unsigned long long*)arena.get(sizeof(unsigned long long) * nrows);
     if (d_seed) CUDA_TRY(cudaMemsetAsync(d_seed, 0, sizeof(unsigned long long) * nrows, st));
   }
-  a.seed = (d_heads || !SYM) ? d_seed : nullptr;
+  if (SELF && in.seed_corr && !F32) {
+    // external row lower bounds (corr units): exact evaluations of admissible
+    // cells, lowered by seed_margin so the sweep's own value of that cell
+    // stays above them (k_seed_fold)
+    if (!d_seed) {
+      d_seed = (unsigned long long*)arena.get(sizeof(unsigned long long) * nrows);
+      if (!d_seed) {
+        if (err) *err = Error{kCudaError, "device allocation failed for the row seeds"};
+        return kCudaError;
+      }
+      CUDA_TRY(cudaMemsetAsync(d_seed, 0, sizeof(unsigned long long) * nrows, st));
+    }
+    k_seed_fold<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(d_seed, in.seed_corr, in.rows.invn, in.rows.flag,
+                                                                  nrows, in.seed_margin);
+    ++nl;
+  }
+  a.seed = (d_heads || !SYM || (SELF && in.seed_corr && !F32)) ? d_seed : nullptr;
   a.tedge = d_te;
   a.tstride = tstride;
   a.tasks = d_tasks;

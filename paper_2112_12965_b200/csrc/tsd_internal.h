@@ -108,6 +108,11 @@ struct JoinInputs {
   // around the join kernel (recorded when non-null); heads_used set by run_join
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   mutable bool heads_used = false;
+  // self-join: optional per-row lower bounds of the best correlation (device,
+  // nrows; <= -2 = none), each an evaluation of an admissible cell; the sweep
+  // starts each row at (bound - seed_margin)
+  const double* seed_corr = nullptr;
+  double seed_margin = 0.0;
 };
 
 // Runs the row-band join of every row against every valid column of every
