@@ -1527,11 +1527,14 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   // segments). Cost model in FP64-op units per warp: a band sweeps its
   // group's cells (3 ops) plus one m-term head per row per segment; the first
   // band of a task also computes the group's top edge (m terms per column).
-  // Tasks are handed out dynamically: several waves cost the total over all
-  // warps plus half a task (the tail); a single wave costs one task over the
-  // fraction of warps it fills (the SMs are issue-bound, and its slowest task
-  // sets the end). G > 1 costs a merge pass. Calibrated on C4 and C2:
-  // profiles/README.md.
+  // Tasks are handed out dynamically, group-major: several waves cost the
+  // total over all warps plus half a task (the tail); a single wave costs one
+  // task over the fraction of warps it fills (the SMs are issue-bound, and its
+  // slowest task sets the end) plus 8 %: uneven progress across SMs is not
+  // rebalanced, and no group starts from the bests an earlier group published.
+  // G > 1 costs a merge pass (16 B per row and group). At most 32 groups and
+  // 16 waves. Calibrated on C4 (G = 16, 28 bands per task: 633 -> 588 ms)
+  // and C2: profiles/README.md.
   int64_t total_cols = 0;
   for (const auto& s : segs) total_cols += s.ncol;
   auto split = [&](int G, std::vector<int>& gs) {
@@ -1550,7 +1553,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   {
     double best = 1e300;
     std::vector<int> gs;
-    for (int g = 1; g <= nseg && g <= 256; g *= 2) {
+    for (int g = 1; g <= nseg && g <= 32; g *= 2) {
       split(g, gs);
       int64_t cmax = 0, smax = 0;
       for (int q = 0; q < g; ++q) {
@@ -1568,9 +1571,10 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       const int bmax = std::min(nbands, F32 ? 4096 / H : 4096);
       for (int b = 1; b <= bmax; ++b) {
         const int64_t nt = (int64_t)((nbands + b - 1) / b) * g;
+        if (nt > 16 * (int64_t)nwarps) continue;
         const double tc = b * band + top;
-        const double run = nt <= nwarps ? tc * nwarps / (double)nt : (double)nt * tc / nwarps + 0.5 * tc;
-        const double cost = run + (g > 1 ? 2e3 * (double)nrows * g / nwarps : 0.0);
+        const double run = nt <= nwarps ? 1.08 * tc * nwarps / (double)nt : (double)nt * tc / nwarps + 0.5 * tc;
+        const double cost = run + (g > 1 ? 30.0 * (double)nrows * g / nwarps : 0.0);
         if (cost < best * 0.999) {
           best = cost;
           G = g;
