@@ -366,6 +366,8 @@ def self_join_lines(q, dist=None, world=1):
             tsd.self_join(x, m, excl=excl)
             ts.append(time.perf_counter() - t0)
         t = statistics.median(ts)
+        if os.environ.get("TSD_BENCH_DEBUG"):
+            print(f"[bench] {name}: {[round(v * 1e3, 2) for v in ts]} ms", file=sys.stderr, flush=True)
         out[name] = {"n": int(x.size), "m": m, "excl": e, "pairs": pairs, "ms": t * 1e3,
                      "value": pairs / t / 1e9, "unit": "GPair/s",
                      "kernel": "symmetric upper-triangle sweep" if cnt >= 450000 else "full-matrix sweep"}

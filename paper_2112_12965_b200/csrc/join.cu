@@ -110,14 +110,17 @@ template <int R>
 struct __align__(16) WarpSmem {
   double4 colbuf[3][32];
   double ering[96];
-  double cring[96];   // SYM: column thresholds (cthr snapshot), same ring layout as ering
-  double inva[R][32];  // SYM: invn_a of each slot's row (column-side candidates)
+  // SYM-only members (the symmetric sweep is the FP64 R = 8 kernel; the FP32
+  // R = 16 layout keeps them as stubs to fit 8 CTAs per SM)
+  static constexpr int NSYM = R == 8 ? 1 : 0;
+  double cring[NSYM ? 96 : 1];   // SYM: column thresholds (cthr snapshot), same ring layout as ering
+  double inva[NSYM ? R : 1][32];  // SYM: invn_a of each slot's row (column-side candidates)
   // SYM: column candidates found since the last chunk turn ({order key, row,
   // col}; at most 40: a segment's last chunk has no turn), merged into ccand
   // at the next turn or at the segment end, one lane per entry
-  unsigned long long cq_key[48];
-  unsigned cq_row[48];
-  int cq_col[48];
+  unsigned long long cq_key[NSYM ? 48 : 1];
+  unsigned cq_row[NSYM ? 48 : 1];
+  int cq_col[NSYM ? 48 : 1];
   int cq_n;
   double bK[R][32];  // best K = cov * invn_b per slot (row factor invn_a left out); +inf = inactive row
   int bj[R][32];     // its concatenated column
@@ -695,15 +698,20 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
 }
 
 // ===========================================================================
-// FP32 mode: the same sweep with the normalised recurrence in packed
-// fma.rn.f32x2 / mul.rn.f32x2 (FFMA2: two slots per instruction). Window
-// statistics, heads and top edges stay FP64 and are rounded once; diagonals
-// restart from an FP64 head at every segment start and every task top, and
-// tasks are capped at 4096 rows, which bounds the FP32 drift.
-// Slot values live in 4 register pairs by physical index; because the slot
-// -> physical map rotates by one per step, the row data is kept in two
-// pairings: A = {(0,1),(2,3),(4,5),(6,7)} (even phase), B = {(1,2),(3,4),
-// (5,6),(7,0)} (odd phase).
+// FP32 mode: the same sweep with the column-normalised recurrence
+//   c~(i, k) = c~(i-1, k-1) * (s_k / s_{k-1}) + (df_a dg_b + dg_a df_b) * s_k,
+// s_k = invn_b[k], in packed fma.rn.f32x2 / mul.rn.f32x2 (FFMA2: two cells per
+// instruction). Window statistics, heads and top edges stay FP64 and are
+// rounded once; diagonals restart from an FP64 head at every segment start and
+// every task top, and tasks are capped at 4096 rows, which bounds the FP32
+// drift.
+// A lane owns 16 consecutive rows (R = 16, bands of 512 rows). Physical
+// register pair q holds the slots (a, a + 8), a = (q - ph) mod 8: both halves
+// move down one slot per step in lockstep, so the rotation is pure register
+// renaming and every FFMA2 reads aligned pairs (no repacking moves). Per step
+// the slot-8 half takes the lane's own slot-7 value and the slot-0 half the
+// previous lane's slot-15 value (one 32-bit shuffle; lane 0 reads the band
+// above through the edge ring, lane 31's slot 15 is the band's bottom row).
 // ===========================================================================
 typedef unsigned long long u64;
 
@@ -742,42 +750,50 @@ struct StepIn32 {
   float e, in;
 };
 
-__device__ __forceinline__ void prefetch32(const Col32* cb, const float* ep, float v7, StepIn32& d) {
+__device__ __forceinline__ void prefetch32(const Col32* cb, const float* ep, float v15, StepIn32& d) {
   const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(cb);
   d.dg2 = a.x;
   d.df2 = a.y;
   d.rk2 = cb->rk2;
   d.e = *ep;
-  d.in = shfl_up1f(v7);
+  d.in = shfl_up1f(v15);
 }
+
+constexpr int R32 = 16;  // rows per lane in the FP32 sweep
 
 struct SweepState32 {
-  u64 Q[4];       // slot values by physical index (pairs)
-  float bK[8];    // best K per slot
-  int thr[8];
+  u64 Q[8];       // physical pair q: slots ((q - ph) & 7, +8)
+  int thr[R32];   // slot_thr32(best K); the bests themselves live in sm.bK
   StepIn32 nx;
+  bool dirty;     // some best changed in this block: refresh thr at its end
 };
 
-__device__ __forceinline__ float qget(const u64 (&Q)[4], int q) { return (q & 1) ? hi2(Q[q >> 1]) : lo2(Q[q >> 1]); }
-__device__ __forceinline__ void qset(u64 (&Q)[4], int q, float v) {
-  Q[q >> 1] = (q & 1) ? pack2(lo2(Q[q >> 1]), v) : pack2(v, hi2(Q[q >> 1]));
-}
-
-__device__ __forceinline__ bool vote_any8f(const u64 (&Q)[4], int ph, const int (&thr)[8]) {
-  int h[8];
+// warp vote over the 16 slot tests "bits(c~) >= thr" (four 4-deep predicate chains)
+__device__ __forceinline__ bool vote_any16f(const u64 (&Q)[8], int ph, const int (&thr)[R32]) {
+  int h[R32];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) h[(q - ph + 8) & 7] = __float_as_int(qget(Q, q));  // slot order
+  for (int q = 0; q < 8; ++q) {
+    const int a = (q - ph + 8) & 7;  // slot order
+    h[a] = (int)(unsigned)Q[q];
+    h[a + 8] = (int)(unsigned)(Q[q] >> 32);
+  }
   unsigned r;
   asm volatile(
-      "{\n .reg .pred a, b;\n"
-      " setp.ge.s32 a, %1, %9;\n setp.ge.s32 b, %5, %13;\n"
-      " setp.ge.or.s32 a, %2, %10, a;\n setp.ge.or.s32 b, %6, %14, b;\n"
-      " setp.ge.or.s32 a, %3, %11, a;\n setp.ge.or.s32 b, %7, %15, b;\n"
-      " setp.ge.or.s32 a, %4, %12, a;\n setp.ge.or.s32 b, %8, %16, b;\n"
-      " or.pred a, a, b;\n vote.sync.any.pred a, a, -1;\n selp.u32 %0, 1, 0, a;\n}\n"
+      "{\n .reg .pred a, b, c, d;\n"
+      " setp.ge.s32 a, %1, %17;\n setp.ge.s32 b, %5, %21;\n setp.ge.s32 c, %9, %25;\n setp.ge.s32 d, %13, %29;\n"
+      " setp.ge.or.s32 a, %2, %18, a;\n setp.ge.or.s32 b, %6, %22, b;\n"
+      " setp.ge.or.s32 c, %10, %26, c;\n setp.ge.or.s32 d, %14, %30, d;\n"
+      " setp.ge.or.s32 a, %3, %19, a;\n setp.ge.or.s32 b, %7, %23, b;\n"
+      " setp.ge.or.s32 c, %11, %27, c;\n setp.ge.or.s32 d, %15, %31, d;\n"
+      " setp.ge.or.s32 a, %4, %20, a;\n setp.ge.or.s32 b, %8, %24, b;\n"
+      " setp.ge.or.s32 c, %12, %28, c;\n setp.ge.or.s32 d, %16, %32, d;\n"
+      " or.pred a, a, b;\n or.pred c, c, d;\n or.pred a, a, c;\n"
+      " vote.sync.any.pred a, a, -1;\n selp.u32 %0, 1, 0, a;\n}\n"
       : "=r"(r)
-      : "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]), "r"(thr[0]),
-        "r"(thr[1]), "r"(thr[2]), "r"(thr[3]), "r"(thr[4]), "r"(thr[5]), "r"(thr[6]), "r"(thr[7]));
+      : "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]), "r"(h[8]),
+        "r"(h[9]), "r"(h[10]), "r"(h[11]), "r"(h[12]), "r"(h[13]), "r"(h[14]), "r"(h[15]), "r"(thr[0]),
+        "r"(thr[1]), "r"(thr[2]), "r"(thr[3]), "r"(thr[4]), "r"(thr[5]), "r"(thr[6]), "r"(thr[7]), "r"(thr[8]),
+        "r"(thr[9]), "r"(thr[10]), "r"(thr[11]), "r"(thr[12]), "r"(thr[13]), "r"(thr[14]), "r"(thr[15]));
   return r != 0;
 }
 
@@ -799,63 +815,90 @@ __device__ __forceinline__ void flush_block32(WarpSmem<R>& sm, const SweepCtx& c
   if (j < cx.ncol - 1) reinterpret_cast<float*>(cx.E)[j] = reinterpret_cast<const float*>(sm.ering)[(b % 3) * 32 + lane];
 }
 
+// FP32 exact update of one step, shared by every unrolled step: the lane's 16
+// slot values staged in slot order (sm.slide, pair a at [a][lane]), K = c~ *
+// (invn_b / s_k) against the best in sm.bK (a float value; strict >, columns
+// arrive in increasing order, profiles.hpp:70-77). Returns whether any best
+// of the lane changed.
+template <bool SELF>
+__device__ __noinline__ bool exact_update32(WarpSmem<R32>& sm, int lane, int col, float kf, long long row0,
+                                            long long excl) {
+  bool any = false;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const u64 v = reinterpret_cast<const u64*>(sm.slide)[a * 32 + lane];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = a + 8 * h;
+      const float K = (h ? hi2(v) : lo2(v)) * kf;
+      bool ok = K > (float)sm.bK[r][lane];
+      if (SELF) {
+        const long long d = row0 + r - col;
+        ok = ok && (d > excl || d < -excl);  // profiles.hpp:281-284
+      }
+      if (ok) {
+        sm.bK[r][lane] = (double)K;
+        sm.bj[r][lane] = col;
+        any = true;
+      }
+    }
+  }
+  __syncwarp();
+  return any;
+}
+
+// One block of 8 steps (the rotation period) starting at k0 (k0 % 8 == 0).
+// FA[a] / GA[a]: the packed row data (df_a, dg_a) of slots (a, a + 8).
 template <bool SELF, bool FIRST, bool GUARD>
-__device__ __forceinline__ void sweep_block32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, int k0, int m96,
-                                              SweepState32& S, const u64 (&FA)[4], const u64 (&GA)[4],
-                                              const u64 (&FB)[4], const u64 (&GB)[4], float* sbase, bool l0) {
-  constexpr int R = 8;
+__device__ __forceinline__ void sweep_block32(WarpSmem<R32>& sm, const SweepCtx& cx, int lane, int k0, int m96,
+                                              SweepState32& S, const u64 (&FA)[8], const u64 (&GA)[8], float* sbase,
+                                              bool l0) {
   const int n = cx.ncol;
   const Col32* cflat = reinterpret_cast<const Col32*>(&sm.colbuf[0][0]);
   const Col32* ccur = cflat + m96;
-  const Col32* cnext = cflat + (m96 + R == 96 ? 0 : m96 + R);
+  const Col32* cnext = cflat + (m96 + 8 == 96 ? 0 : m96 + 8);
   const float* ring = reinterpret_cast<const float*>(sm.ering);
   const int ebase = m96;
   float* const st_prev = sbase + (m96 == 0 ? 95 : m96 - 1);
   float* const st_cur = sbase + ebase;
 #pragma unroll
-  for (int u = 0; u < R; ++u) {
+  for (int u = 0; u < 8; ++u) {
     const int k = k0 + u;
     if (GUARD && k >= n) break;
-    const int ph = (R - u) & (R - 1);
+    const int ph = (8 - u) & 7;  // physical pair of slots (0, 8) at this step
     if (!(FIRST && u == 0)) {
-      const float out = qget(S.Q, ph);
-      (u == 0 ? st_prev : st_cur + u - 1)[0] = out;
-      qset(S.Q, ph, l0 ? S.nx.e : S.nx.in);
+      // the pair that held slots (7, 15) now holds (0, 8): lane 31 retires its
+      // slot 15 (bottom row, column k-1); slot 8 takes the lane's own slot 7
+      const u64 old = S.Q[ph];
+      (u == 0 ? st_prev : st_cur + u - 1)[0] = hi2(old);
+      S.Q[ph] = pack2(l0 ? S.nx.e : S.nx.in, lo2(old));
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        // row pair of physical pair p at this phase (A for even, B for odd)
-        const u64 fa = (ph & 1) ? FB[(p - (ph + 1) / 2 + 4) & 3] : FA[(p - ph / 2 + 4) & 3];
-        const u64 ga = (ph & 1) ? GB[(p - (ph + 1) / 2 + 4) & 3] : GA[(p - ph / 2 + 4) & 3];
-        const u64 t = fma2(fa, S.nx.dg2, mul2(ga, S.nx.df2));
-        S.Q[p] = fma2(S.Q[p], S.nx.rk2, t);
+      for (int q = 0; q < 8; ++q) {
+        const int a = (q - ph + 8) & 7;
+        const u64 t = fma2(FA[a], S.nx.dg2, mul2(GA[a], S.nx.df2));
+        S.Q[q] = fma2(S.Q[q], S.nx.rk2, t);
       }
     }
-    if (!GUARD || k + 1 < n) prefetch32(u + 1 < R ? ccur + u + 1 : cnext, &ring[ebase + u], qget(S.Q, (ph + 7) & 7), S.nx);
-    if (vote_any8f(S.Q, ph, S.thr)) [[unlikely]] {
-      const float kf = (ccur + u)->kf;
-      const int col = cx.colbase + k;
+    if (!GUARD || k + 1 < n) prefetch32(u + 1 < 8 ? ccur + u + 1 : cnext, &ring[ebase + u], hi2(S.Q[(ph + 7) & 7]), S.nx);
+    if (vote_any16f(S.Q, ph, S.thr)) [[unlikely]] {
+      // stage the pairs in slot order and run the one shared exact update
+      // (eight inline copies of it would overflow the instruction cache)
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const float K = qget(S.Q, (r + ph) & 7) * kf;
-        bool ok = K > S.bK[r];
-        if (SELF) {
-          const long long d = cx.row0 + r - col;
-          ok = ok && (d > cx.excl || d < -cx.excl);
-        }
-        if (ok) {
-          S.bK[r] = K;
-          sm.bj[r][lane] = col;
-          S.thr[r] = slot_thr32(K);
-        }
-      }
+      for (int q = 0; q < 8; ++q) reinterpret_cast<u64*>(sm.slide)[((q - ph + 8) & 7) * 32 + lane] = S.Q[q];
+      __syncwarp();
+      S.dirty |= exact_update32<SELF>(sm, lane, cx.colbase + k, (ccur + u)->kf, cx.row0, cx.excl);
     }
+  }
+  if (S.dirty) {  // thresholds of the bests this block raised (stale ones only pass more cells)
+#pragma unroll
+    for (int r = 0; r < R32; ++r) S.thr[r] = slot_thr32((float)sm.bK[r][lane]);
+    S.dirty = false;
   }
 }
 
 template <bool SELF>
-__device__ void sweep_segment32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, const u64 (&FA)[4],
-                                const u64 (&GA)[4], const u64 (&FB)[4], const u64 (&GB)[4], SweepState32& S) {
-  constexpr int R = 8;
+__device__ void sweep_segment32(WarpSmem<R32>& sm, const SweepCtx& cx, int lane, const u64 (&FA)[8],
+                                const u64 (&GA)[8], SweepState32& S) {
   const int n = cx.ncol;
   const int nchunks = (n + 31) >> 5;
   float* const sbase = reinterpret_cast<float*>(lane == 31 ? sm.ering : sm.slide + 256);
@@ -868,7 +911,7 @@ __device__ void sweep_segment32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, c
   int flushed = 0;
   if (n > 1)
     prefetch32(reinterpret_cast<const Col32*>(&sm.colbuf[0][1]), reinterpret_cast<const float*>(sm.ering),
-               qget(S.Q, 7), S.nx);
+               hi2(S.Q[7]), S.nx);
   auto chunk_turn = [&](int c) {
     __syncwarp();
     if (c >= 2 && cx.write_out) {
@@ -880,19 +923,19 @@ __device__ void sweep_segment32(WarpSmem<8>& sm, const SweepCtx& cx, int lane, c
     cp_wait<1>();
     __syncwarp();
   };
-  constexpr int BPC = 32 / R;
-  if (n <= R) {
-    sweep_block32<SELF, true, true>(sm, cx, lane, 0, 0, S, FA, GA, FB, GB, sbase, l0);
+  constexpr int BPC = 32 / 8;
+  if (n <= 8) {
+    sweep_block32<SELF, true, true>(sm, cx, lane, 0, 0, S, FA, GA, sbase, l0);
   } else {
-    sweep_block32<SELF, true, false>(sm, cx, lane, 0, 0, S, FA, GA, FB, GB, sbase, l0);
-    int k0 = R, m96 = R, bic = 1;
-    for (; k0 + R <= n; k0 += R) {
-      if (bic == BPC - 1 && k0 + R < n) chunk_turn((k0 + R) >> 5);
-      sweep_block32<SELF, false, false>(sm, cx, lane, k0, m96, S, FA, GA, FB, GB, sbase, l0);
-      m96 = m96 + R == 96 ? 0 : m96 + R;
+    sweep_block32<SELF, true, false>(sm, cx, lane, 0, 0, S, FA, GA, sbase, l0);
+    int k0 = 8, m96 = 8, bic = 1;
+    for (; k0 + 8 <= n; k0 += 8) {
+      if (bic == BPC - 1 && k0 + 8 < n) chunk_turn((k0 + 8) >> 5);
+      sweep_block32<SELF, false, false>(sm, cx, lane, k0, m96, S, FA, GA, sbase, l0);
+      m96 = m96 + 8 == 96 ? 0 : m96 + 8;
       bic = bic == BPC - 1 ? 0 : bic + 1;
     }
-    if (k0 < n) sweep_block32<SELF, false, true>(sm, cx, lane, k0, m96, S, FA, GA, FB, GB, sbase, l0);
+    if (k0 < n) sweep_block32<SELF, false, true>(sm, cx, lane, k0, m96, S, FA, GA, sbase, l0);
   }
   cp_wait<0>();
   __syncwarp();
@@ -1093,14 +1136,15 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           }
         } else {  // left edge: cov(i, col0) for the band's rows, batched 8 segments at a time
 #ifndef TSD_ABL_NOHEADS
-          if (((s - s_beg) & 7) == 0 && a.dmma_heads)
+          if (R == 8 && ((s - s_beg) & 7) == 0 && a.dmma_heads)
 #else
           if (s == s_beg && b == b0)
 #endif
-            heads_dmma<R>(sm, a.xa + i0, a.na - i0, cA, a.btil + (int64_t)s * a.m, min(8, s_end - s), a.m, lane,
-                          Hw);
+            if constexpr (R == 8)
+              heads_dmma<R>(sm, a.xa + i0, a.na - i0, cA, a.btil + (int64_t)s * a.m, min(8, s_end - s), a.m, lane,
+                            Hw);
           double out[R];
-          if (a.dmma_heads) {
+          if (R == 8 && a.dmma_heads) {  // heads_dmma: 256-row bands
 #pragma unroll
             for (int r = 0; r < R; ++r) out[r] = Hw[((s - s_beg) & 7) * 256 + R * lane + r];
           } else {
@@ -1115,7 +1159,8 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           }
         }
         if constexpr (F32) {
-          // row data in both pairings, rounded once
+          // row data of slots (a, a + 8) packed, rounded once
+          static_assert(!F32 || R == R32, "the FP32 sweep runs 16 rows per lane");
           float fa[R], ga[R];
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -1124,27 +1169,23 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
             fa[r] = in ? (float)a.dfa[i] : 0.0f;
             ga[r] = in ? (float)a.dga[i] : 0.0f;
           }
-          u64 FA[4], GA[4], FB[4], GB[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            FA[j] = pack2(fa[2 * j], fa[2 * j + 1]);
-            GA[j] = pack2(ga[2 * j], ga[2 * j + 1]);
-            FB[j] = pack2(fa[2 * j + 1], fa[(2 * j + 2) & 7]);
-            GB[j] = pack2(ga[2 * j + 1], ga[(2 * j + 2) & 7]);
-          }
+          u64 FA[8], GA[8];
           SweepState32 S;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) S.Q[j] = pack2((float)head[2 * j], (float)head[2 * j + 1]);
+          for (int q = 0; q < 8; ++q) {
+            FA[q] = pack2(fa[q], fa[q + 8]);
+            GA[q] = pack2(ga[q], ga[q + 8]);
+            S.Q[q] = pack2((float)head[q], (float)head[q + 8]);
+          }
+          // bests as FP32 values (seeds rounded once; +inf = inactive row)
 #pragma unroll
           for (int r = 0; r < R; ++r) {
-            const double bk = sm.bK[r][lane];
-            S.bK[r] = (float)bk;
-            S.thr[r] = isinf(bk) && bk > 0 ? INT_MAX : slot_thr32(S.bK[r]);
+            const float bk = (float)sm.bK[r][lane];
+            sm.bK[r][lane] = (double)bk;
+            S.thr[r] = slot_thr32(bk);
           }
-          sweep_segment32<SELF>(sm, cx, lane, FA, GA, FB, GB, S);
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-            if (!(isinf(sm.bK[r][lane]) && sm.bK[r][lane] > 0)) sm.bK[r][lane] = (double)S.bK[r];
+          S.dirty = false;
+          if constexpr (R == R32) sweep_segment32<SELF>(sm, cx, lane, FA, GA, S);
         } else {
           SweepState<R> S;
 #pragma unroll
@@ -1809,6 +1850,12 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       }
     }
   }
+  if (getenv("TSD_VERBOSE")) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    fprintf(stderr, "[tsd] heads %s, top edges %s, free %.1f GB\n", d_heads ? "fft" : "in-kernel",
+            d_te ? "fft" : "in-kernel", fr / 1e9);
+  }
   JoinArgs a;
   a.xa = in.xa;
   a.na = in.na;
@@ -1838,7 +1885,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   a.hscr = d_hscr;
   {
     const char* e = getenv("TSD_DMMA_HEADS");
-    a.dmma_heads = SYM ? 0 : (e ? atoi(e) : 1);  // SYM heads sit at band-dependent columns
+    a.dmma_heads = (SYM || R != 8) ? 0 : (e ? atoi(e) : 1);  // SYM heads sit at band-dependent columns
   }
   a.heads = d_heads;
   a.hstride = hstride;
@@ -1962,8 +2009,8 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
              int* launches) {
   const bool self = in.excl >= 0;
   if (in.precision == 1) {
-    const int rc = self ? launch_join<8, true, true, false>(in, d_best_c, d_best_j, arena, st, err, launches)
-                        : launch_join<8, false, true, false>(in, d_best_c, d_best_j, arena, st, err, launches);
+    const int rc = self ? launch_join<R32, true, true, false>(in, d_best_c, d_best_j, arena, st, err, launches)
+                        : launch_join<R32, false, true, false>(in, d_best_c, d_best_j, arena, st, err, launches);
     if (rc != kOk) return rc;
     const int64_t n = in.rows.nwin;
     k_refine_fp64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_best_c, d_best_j, n, in.xa, in.rows.mu,

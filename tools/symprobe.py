@@ -8,6 +8,8 @@ import paper_2112_12965_b200 as t
 from paper_2112_12965_b200 import synth
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 cases = [("C2", synth.ecg(2, 131072)[0], 250, 62), ("w21", synth.walk(4, 1 << 21), 512, None)]
+if os.environ.get("REV"):
+    cases = cases[::-1]
 if os.environ.get("ONLY"):
     cases = [c for c in cases if c[0] == os.environ["ONLY"]]
 for name, x, m, excl in cases:
