@@ -273,6 +273,8 @@ def run_gpu(args):
     # sanity: the e2e result equals the device-resident result
     same = bool(torch.equal(h_idx, d_idx.cpu())) and bool(torch.equal(h_val, d_val.cpu()))
 
+    plan.close()  # release the FP64 plan's device arenas before the FP32 plan
+    fp32 = fp32_line(D, d_q, d_val, d_idx, stream, flush, dev, dist, world)
     sj = self_join_lines(q, dist, world)  # every rank (the sharded run needs all of them)
     if rank != 0:
         if dist:
@@ -309,6 +311,7 @@ def run_gpu(args):
                     "d2h_bytes_per_step": int(nrows * 16), "api": "tsd_dict_join (host buffers, pinned)",
                     "matches_device_path": same},
             "gpu_launches": launches, "clocks": clk.summary(),
+            "fp32": fp32,
             "self_join": sj,
             "join_ms_median": jms, "fraction_of_fp64_peak_cells": (cells_per_step() / (jms * 1e-3)) /
                                                                     (peak / FLOPS_PER_CELL)}
@@ -316,6 +319,50 @@ def run_gpu(args):
     if dist:
         dist.destroy_process_group()
     return 0
+
+
+def fp32_line(D, d_q, d_val, d_idx, stream, flush, dev, dist=None, world=1, steps=3, warmup=3):
+    """BASELINE C4 in the optional FP32 mode (north star: distances within
+    1e-3 absolute): the same device-resident step, with the join kernel's
+    achieved fraction of the FP32 cell roofline (6 FP32 flops per cell at the
+    FFMA peak measured live). Timed like the FP64 line (CUDA events on the
+    launching stream, L2 flushed between steps, max over ranks)."""
+    import torch
+    import paper_2112_12965_b200 as tsd
+    plan = tsd.DictPlan(D, M, "fp32")
+
+    def step():
+        plan.join_device(d_q.data_ptr(), [Q_LEN], d_val.data_ptr(), d_idx.data_ptr(), stream.cuda_stream)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if dist:
+        dist.barrier()
+    ms, kms = 0.0, []
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        ms += e0.elapsed_time(e1)
+        kms.append(plan.last_kernel_timing()[0])
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    plan.close()
+    peak32 = tsd.measure_peak("fp32", seconds=1.0)
+    k = statistics.median(kms)
+    return {"value": cells_per_step() * world * steps / (ms * 1e-3) / 1e9, "unit": "GCell/s",
+            "ms_per_step": ms / steps, "dtype": "f32 sweep, FP64 statistics / heads / final correlation",
+            "roofline": {"bound": "fp32", "achieved": FLOPS_PER_CELL * cells_per_step() / (k * 1e-3) / 1e12,
+                         "peak": peak32 / 1e12, "unit": "TFLOP/s",
+                         "frac": FLOPS_PER_CELL * cells_per_step() / (k * 1e-3) / peak32,
+                         "kernel": "k_join<16,false,true> (FP32 f32x2 row-band join)",
+                         "peak_def": "FFMA throughput measured live by tsd_measure_peak (1 s, this GPU)"}}
 
 
 def self_join_lines(q, dist=None, world=1):
@@ -360,7 +407,7 @@ def self_join_lines(q, dist=None, world=1):
         pairs = (cnt - e - 1) * (cnt - e) / 2
         tsd.self_join(x, m, excl=excl)  # warm
         ts = []
-        for _ in range(3):
+        for _ in range(5):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             tsd.self_join(x, m, excl=excl)

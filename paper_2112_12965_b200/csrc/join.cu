@@ -502,7 +502,50 @@ struct SweepState {
   double bKp[R];  // kplus(bestK); bestK itself and its column live in sm.bK / sm.bj
   int thr[R];     // hi(bKp * nmin) of the current block
   StepIn nx;      // prefetched inputs of the next step
+  bool dirty;     // (warp-uniform) a best changed: reload bKp at the next threshold block
 };
+
+// FP64 exact update of one step (AB / full-matrix self-join), shared by every
+// unrolled step so the sweep loop stays small in the instruction cache: the
+// lane's slot covariances staged in slot order (sm.slide[r * 32 + lane]),
+// K = cov * invn_b against the best in sm.bK, strict > (columns arrive in
+// increasing order, so ties keep the lower column, profiles.hpp:70-77; a flat
+// column has invn_b = 0 -> K = 0, :332-336). Returns whether any best of the
+// warp changed.
+template <int R, bool SELF>
+__device__ __noinline__ bool exact_update64(WarpSmem<R>& sm, int lane, int col, double invb, long long row0,
+                                            long long excl) {
+  bool any = false;
+#ifdef TSD_COUNT_EXACT
+  int nupd = 0;
+#endif
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const double K = sm.slide[r * 32 + lane] * invb;
+    bool ok = K > sm.bK[r][lane];
+    if (SELF) {
+      const long long d = row0 + r - col;
+      ok = ok && (d > excl || d < -excl);  // profiles.hpp:281-284
+    }
+    if (ok) {
+      sm.bK[r][lane] = K;
+      sm.bj[r][lane] = col;
+      any = true;
+    }
+#ifdef TSD_COUNT_EXACT
+    nupd += ok;
+#endif
+  }
+#ifdef TSD_COUNT_EXACT
+  {
+    const unsigned anyu = __ballot_sync(0xffffffffu, nupd > 0);
+    for (int o = 16; o; o >>= 1) nupd += __shfl_xor_sync(0xffffffffu, nupd, o);
+    if (lane == 0 && anyu) atomicAdd(&g_true_steps, 1ull);
+    if (lane == 0) atomicAdd(&g_true_slots, (unsigned long long)nupd);
+  }
+#endif
+  return __any_sync(0xffffffffu, any);
+}
 
 // One block of R steps starting at k0 (k0 % R == 0, R | 32). FIRST: block 0,
 // whose step 0 (heads, already in P) only needs its test. GUARD: steps may
@@ -531,6 +574,11 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
     const int ph = (R - u) & (R - 1);  // physical register of slot 0 at this step
     if (u % TB == 0) {  // threshold block of TB columns (nmin prefetched with its first column)
       nmin = (FIRST && u == 0) ? ccur[0].w : S.nx.nmin;
+      if (!SYM && S.dirty) {  // bests raised by the shared exact update since the last block
+#pragma unroll
+        for (int r = 0; r < R; ++r) S.bKp[r] = kplus(sm.bK[r][lane]);
+        S.dirty = false;
+      }
 #ifdef TSD_ABL_NOCOLFOLD
       if (false) {
 #else
@@ -592,35 +640,12 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
             }
         }
       } else {
-#ifdef TSD_COUNT_EXACT
-      int nupd = 0;
-#endif
+        // stage the slot values in slot order for the shared exact update;
+        // the thresholds of raised bests are refreshed at the next threshold
+        // block (stale ones only let more cells through to the exact test)
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const double K = S.P[(r + ph) & (R - 1)] * invb;
-        bool ok = K > sm.bK[r][lane];
-        if (SELF) {
-          const long long d = cx.row0 + r - col;
-          ok = ok && (d > cx.excl || d < -cx.excl);  // profiles.hpp:281-284
-        }
-        if (ok) {
-          sm.bK[r][lane] = K;
-          sm.bj[r][lane] = col;
-          S.bKp[r] = kplus(K);
-          S.thr[r] = __double2hiint(S.bKp[r] * nmin);
-        }
-#ifdef TSD_COUNT_EXACT
-        nupd += ok;
-#endif
-      }
-#ifdef TSD_COUNT_EXACT
-      {
-        const unsigned any = __ballot_sync(0xffffffffu, nupd > 0);
-        for (int o = 16; o; o >>= 1) nupd += __shfl_xor_sync(0xffffffffu, nupd, o);
-        if (lane == 0 && any) atomicAdd(&g_true_steps, 1ull);
-        if (lane == 0) atomicAdd(&g_true_slots, (unsigned long long)nupd);
-      }
-#endif
+        for (int r = 0; r < R; ++r) sm.slide[r * 32 + lane] = S.P[(r + ph) & (R - 1)];
+        S.dirty |= exact_update64<R, SELF>(sm, lane, col, invb, cx.row0, cx.excl);
       }
     }
   }
@@ -885,7 +910,6 @@ __device__ __forceinline__ void sweep_block32(WarpSmem<R32>& sm, const SweepCtx&
       // (eight inline copies of it would overflow the instruction cache)
 #pragma unroll
       for (int q = 0; q < 8; ++q) reinterpret_cast<u64*>(sm.slide)[((q - ph + 8) & 7) * 32 + lane] = S.Q[q];
-      __syncwarp();
       S.dirty |= exact_update32<SELF>(sm, lane, cx.colbase + k, (ccur + u)->kf, cx.row0, cx.excl);
     }
   }
@@ -1188,6 +1212,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           if constexpr (R == R32) sweep_segment32<SELF>(sm, cx, lane, FA, GA, S);
         } else {
           SweepState<R> S;
+          S.dirty = false;
 #pragma unroll
           for (int r = 0; r < R; ++r) S.P[r] = head[r];
           // row data and row bests (reloaded per segment so they are not live
