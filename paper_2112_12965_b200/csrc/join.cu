@@ -37,6 +37,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <type_traits>
 
 #include "tsd_common.cuh"
 #include "tsd_internal.h"
@@ -114,19 +115,29 @@ struct __align__(16) WarpSmem {
   // R = 16 layout keeps them as stubs to fit 8 CTAs per SM)
   static constexpr int NSYM = R == 8 ? 1 : 0;
   double cring[NSYM ? 96 : 1];   // SYM: column thresholds (cthr snapshot), same ring layout as ering
+  double cminb[NSYM ? 24 : 1];   // SYM: weakest column threshold of each 4-column block of the ring
   double inva[NSYM ? R : 1][32];  // SYM: invn_a of each slot's row (column-side candidates)
   // SYM: column candidates found since the last chunk turn ({order key, row,
-  // col}; at most 40: a segment's last chunk has no turn), merged into ccand
-  // at the next turn or at the segment end, one lane per entry
-  unsigned long long cq_key[NSYM ? 48 : 1];
-  unsigned cq_row[NSYM ? 48 : 1];
-  int cq_col[NSYM ? 48 : 1];
+  // col}; at most 40 = the 8 steps after the last turn plus a segment's last
+  // chunk, which has no turn), merged into ccand at the next turn or at the
+  // segment end, one lane per entry. (Sizes matter: 8 two-warp CTAs per SM
+  // leave 14080 B per warp.)
+  unsigned long long cq_key[NSYM ? 40 : 1];
+  unsigned cq_row[NSYM ? 40 : 1];
+  int cq_col[NSYM ? 40 : 1];
   int cq_n;
-  double bK[R][32];  // best K = cov * invn_b per slot (row factor invn_a left out); +inf = inactive row
+  // best K = cov * invn_b per slot (row factor invn_a left out); +inf =
+  // inactive row. The FP32 sweep (R = 16) keeps FP32 bests: float storage
+  // fits its 16 rows per lane in 8 CTAs per SM
+  std::conditional_t<R == 8, double, float> bK[R][32];
   int bj[R][32];     // its concatenated column
   double slide[Geo<R>::SLIDE];
   double unif[T];
 };
+
+// 8 two-warp CTAs per SM: 233472 B of shared memory less 1 KiB reserved per CTA
+static_assert(sizeof(WarpSmem<8>) <= 14080 && sizeof(WarpSmem<16>) <= 14080,
+              "per-warp shared memory must fit 8 two-warp CTAs per SM");
 
 #ifdef TSD_COUNT_EXACT
 __device__ unsigned long long g_exact_count, g_step_count, g_exact_first, g_step_first, g_col_count, g_cas_count,
@@ -313,6 +324,17 @@ __device__ __forceinline__ void issue_chunk(WarpSmem<R>& sm, const SweepCtx& cx,
   if (lane < 16) cp16(&sm.ering[(c % 3) * 32 + 2 * lane], cx.E + 32 * c + 2 * lane);
   else if (cx.cthr) cp16(&sm.cring[(c % 3) * 32 + 2 * (lane - 16)], cx.cthr + 32 * c + 2 * (lane - 16));
   cp_commit();
+}
+
+// SYM: once chunk c is resident, the weakest threshold of each of its eight
+// 4-column blocks (one lane per block)
+template <int R>
+__device__ __forceinline__ void fold_cmin(WarpSmem<R>& sm, int lane, int c) {
+  if (lane < 8) {
+    const double* t = &sm.cring[(c % 3) * 32 + 4 * lane];
+    sm.cminb[(c % 3) * 8 + lane] = fmin(fmin(t[0], t[1]), fmin(t[2], t[3]));
+  }
+  __syncwarp();
 }
 
 template <int R>
@@ -584,10 +606,8 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
 #else
       if (SYM) {  // column side folded in: the block's weakest column threshold
 #endif
-        double cmin = sm.cring[ebase + u];
-#pragma unroll
-        for (int t = 1; t < TB; ++t) cmin = fmin(cmin, sm.cring[ebase + u + t]);
-        tcb = __double2hiint(cmin * cx.namin);
+        static_assert(TB == 4, "cminb folds 4-column blocks");
+        tcb = __double2hiint(sm.cminb[(ebase + u) >> 2] * cx.namin);
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) S.thr[r] = SYM ? min(__double2hiint(S.bKp[r] * nmin), tcb)
@@ -671,6 +691,7 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   if (nchunks > 1) issue_chunk(sm, cx, lane, 1); else cp_commit();
   cp_wait<1>();
   __syncwarp();
+  if (SYM) fold_cmin(sm, lane, 0);
   int flushed = 0;  // edge blocks [0, flushed) written back
   // blocks of R steps; every 32 / R blocks the next block opens chunk c:
   // make it resident, retire edge block c-2, start loading chunk c+1 (3-deep
@@ -688,6 +709,7 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
     cp_wait<1>();
 #endif
     __syncwarp();
+    if (SYM) fold_cmin(sm, lane, c);
   };
   constexpr int BPC = 32 / R;  // blocks per chunk
   if (n <= R) {
