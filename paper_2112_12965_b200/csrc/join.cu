@@ -1261,12 +1261,21 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
         const int64_t i = i0 + R * lane + r;
         if (i < a.nrows) {
           const int j = sm.bj[r][lane];
-          oc[i] = j >= 0 ? clamp_corr(sm.bK[r][lane] * a.invn_a[i]) : -2.0;
+          const double c = j >= 0 ? clamp_corr(sm.bK[r][lane] * a.invn_a[i]) : -2.0;
+          oc[i] = c;
           oj[i] = j;
           // publish the band's best: later tasks on these rows (other groups)
           // start from it. It is exactly the K this group's sweep computed for
           // the recorded cell, so the seed argument above holds for it too.
           if (!SYM && j >= 0 && a.seed) atomicMax(a.seed + i, order_key(sm.bK[r][lane]));
+          // SYM: the row's best so far bounds its final best from below, so it
+          // raises the column-side threshold of column i (same window): in
+          // clamped correlation units like col_update, lowered by 2^-40, so a
+          // lower-triangle candidate tying with it still passes
+          if (SYM && j >= 0) {
+            const double t = kplus_d(c) * (1.0 / a.invn_a[i]) * (1.0 - 0x1p-40);
+            atomicMax(reinterpret_cast<long long*>(a.cthr + i), __double_as_longlong(t));
+          }
         }
       }
       __syncwarp();
