@@ -261,6 +261,9 @@ int plan_join_host(tsd_dict_plan* p, const double* q, const size_t* q_len, size_
   verbose_phase("query upload", st, t0);
   if (int rc = plan_join_dev(p, d_q, q_len, nser, d_val, d_idx, st)) return rc;
   verbose_phase("join", st, t0);
+  if (getenv("TSD_VERBOSE"))
+    fprintf(stderr, "[tsd] device: step %.2f ms, join %.2f ms, kernel %.2f ms, heads %.2f ms\n", p->step_ms, p->join_ms,
+            p->kernel_ms, p->heads_ms);
   CK(cudaMemcpyAsync(val, d_val, sizeof(double) * outn, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(idx, d_idx, sizeof(int64_t) * outn, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

@@ -596,7 +596,7 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
     const int ph = (R - u) & (R - 1);  // physical register of slot 0 at this step
     if (u % TB == 0) {  // threshold block of TB columns (nmin prefetched with its first column)
       nmin = (FIRST && u == 0) ? ccur[0].w : S.nx.nmin;
-      if (!SYM && S.dirty) {  // bests raised by the shared exact update since the last block
+      if (S.dirty) {  // bests raised by the shared exact update since the last block
 #pragma unroll
         for (int r = 0; r < R; ++r) S.bKp[r] = kplus(sm.bK[r][lane]);
         S.dirty = false;
@@ -650,15 +650,9 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
         const int tc = __double2hiint(sm.cring[ebase + u] * cx.namin);  // this column's own threshold
         const unsigned upd =
             exact_update_sym<R>(sm, lane, col, invb, tc, (int)cx.row0, (int)cx.excl, cthr);
-        __syncwarp();
-        if (upd) {
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-            if ((upd >> r) & 1u) {
-              S.bKp[r] = kplus(sm.bK[r][lane]);
-              S.thr[r] = min(__double2hiint(S.bKp[r] * nmin), tcb);
-            }
-        }
+        // raised row bests: their thresholds are refreshed at the next
+        // threshold block, as in the AB sweep
+        S.dirty |= __any_sync(0xffffffffu, upd != 0);
       } else {
         // stage the slot values in slot order for the shared exact update;
         // the thresholds of raised bests are refreshed at the next threshold
@@ -1589,6 +1583,13 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   // masks and the epilogue's source mapping are unchanged; each piece starts
   // from its own head (cov at its first column), exactly as a segment does.
   const auto t_host0 = std::chrono::steady_clock::now();
+  static const bool vmarks = getenv("TSD_VERBOSE") && getenv("TSD_VMARKS");
+  auto vmark = [&](const char* what) {  // development timing: host time, stream drained
+    if (!vmarks) return;
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[tsd]   %s at %.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_host0).count());
+  };
   std::vector<SegDev> vsegs;
   {
     int64_t tot = 0;
@@ -1613,6 +1614,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem_bytes = sizeof(WarpSmem<R>) * WARPS;
   auto kern = k_join<R, SELF, F32, SYM>;
+  vmark("segments");
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * WARPS, smem_bytes);
@@ -1632,6 +1634,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   // G > 1 costs a merge pass (16 B per row and group). At most 32 groups and
   // 16 waves. Calibrated on C4 (G = 16, 28 bands per task: 633 -> 588 ms)
   // and C2: profiles/README.md.
+  vmark("occupancy");
   int64_t total_cols = 0;
   for (const auto& s : segs) total_cols += s.ncol;
   auto split = [&](int G, std::vector<int>& gs) {
@@ -1855,6 +1858,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   ++nl;
   k_btil<<<nseg, 128, 0, st>>>(in.xb, in.cols.mu, d_segs, m, d_btil, d_ebt);
   ++nl;
+  vmark("allocations + packing");
   // heads by FFT correlation when there are several segments and the
   // [seg][row] array fits comfortably (C4: 256 x 2^24 doubles = 34 GB)
   const int64_t hstride = (int64_t)nbands * H;
@@ -1880,6 +1884,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       }
     }
   }
+  vmark("heads fft");
   // top edges by FFT: one row of the table per band range, all columns
   double* d_te = nullptr;
   int64_t tstride = 0;
@@ -1912,6 +1917,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     fprintf(stderr, "[tsd] heads %s, top edges %s, free %.1f GB\n", d_heads ? "fft" : "in-kernel",
             d_te ? "fft" : "in-kernel", fr / 1e9);
   }
+  vmark("top edges fft");
   JoinArgs a;
   a.xa = in.xa;
   a.na = in.na;
@@ -1994,7 +2000,9 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   cudaMemcpyToSymbol(g_true_slots, &zero, 8);
 #endif
   if (in.ev[2]) CUDA_TRY(cudaEventRecord(in.ev[2], st));
+  vmark("args + sym init");
   kern<<<grid, 32 * WARPS, smem_bytes, st>>>(a);
+  vmark("k_join");
   ++nl;
   if (in.ev[3]) CUDA_TRY(cudaEventRecord(in.ev[3], st));
 #ifdef TSD_COUNT_EXACT
