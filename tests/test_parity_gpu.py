@@ -450,6 +450,28 @@ def test_fp32_mode_self_join_and_flat():
     check_profile(P.values, P.indices, rv, ri, 64, ab_dist(a, b, 64), fp32=True, label="fp32 flat")
 
 
+@pytest.mark.parametrize("nq", [64 + 1, 64 + 7, 64 + 511, 64 + 512, 64 + 513, 64 + 4097])
+def test_fp32_ragged_bands_and_segments(nq):
+    """The FP32 sweep's 16-row lanes and 512-row bands against the oracle on
+    ragged shapes: a single row, partial bands, exactly one band, one row
+    past it, more rows than one 4096-row task; segments of 1, 7, 8, 9, 33
+    and 300 windows (guarded 8-step blocks, chunk edges, several chunks)."""
+    m = 64
+    q = synth.walk(70 + nq, nq)
+    lens = [m, m + 6, m + 7, m + 8, m + 32, m + 299]
+    segs = [synth.walk(80 + k, L) for k, L in enumerate(lens)]
+    starts = list(np.cumsum([0] + [L + 5 for L in lens[:-1]]))
+    P = tsd.join_dictionary(q, _dict(segs, starts, m), m, precision="fp32")
+    rv, ri = O.dict_join(q, segs, starts, m)
+    st = check_profile(P.values, P.indices, rv, ri, m, dict_dist(q, segs, starts, m), fp32=True,
+                       label=f"fp32 ragged nq={nq}")
+    assert st["max_abs"] <= 1e-3
+    if nq >= 2 * m:
+        P = tsd.self_join(q, m, excl=m // 4, precision="fp32")
+        rv, ri = O.self_join(q, m, m // 4)
+        check_profile(P.values, P.indices, rv, ri, m, ab_dist(q, q, m), fp32=True, label=f"fp32 self nq={nq}")
+
+
 # ------------------------------------------------------------- greedy learning (SURVEY 8(f) rank 1)
 def _learn_cfg(c):
     rule, value = int(c["rule"]), float(c["value"])
