@@ -355,6 +355,16 @@ __device__ __forceinline__ void flush_block(WarpSmem<R>& sm, const SweepCtx& cx,
 // (1 - 2^-40) staged per chunk. A pass reduces the warp's best (corr, row)
 // (max corr, lowest row) and merges it into ccand[j] with a 128-bit CAS.
 __device__ __forceinline__ double kplus_d(double b) { return b > 0.0 ? b : -0.0; }
+// 1/x for positive normal x without the division's divergent slow-path call
+// (which would make the compiler guard every later shuffle and vote of the
+// sweep with divergence checks): approximate reciprocal + two Newton steps,
+// within an ulp or two -- used only inside thresholds that carry a 2^-40 slack
+__device__ __forceinline__ double rcp_pos(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = __fma_rn(r, __fma_rn(-x, r, 1.0), r);
+  return __fma_rn(r, __fma_rn(-x, r, 1.0), r);
+}
 // SYM column candidates are spread over SYM_NC copies (by task) so that the
 // many bands sweeping the same columns at once do not serialise on one CAS
 // target; the copies are merged per row after the join
@@ -418,7 +428,7 @@ __device__ __noinline__ void col_update(WarpSmem<R>& sm, int lane, unsigned cm, 
     // raise the column threshold now (a real pair's value never exceeds the
     // row's final best; non-returning atomic) and queue the (corr, row)
     // candidate for the 128-bit merge at the next chunk turn
-    const double t = kplus_d(key_value(wk)) * (1.0 / invb) * (1.0 - 0x1p-40);
+    const double t = kplus_d(key_value(wk)) * rcp_pos(invb) * (1.0 - 0x1p-40);
     atomicMax(reinterpret_cast<long long*>(cthr + col), __double_as_longlong(t));
     const int q = sm.cq_n;
     sm.cq_key[q] = wk;
@@ -433,18 +443,35 @@ __device__ __noinline__ void col_update(WarpSmem<R>& sm, int lane, unsigned cm, 
 template <int R>
 __device__ __noinline__ void col_flush(WarpSmem<R>& sm, int lane, unsigned long long* ccand) {
   __syncwarp();
-  const int nq = sm.cq_n;
-  for (int e = lane; e < nq; e += 32) {
-    const long long col = sm.cq_col[e];
-    unsigned long long* p = ccand + 2 * col;
-    const unsigned long long nk = sm.cq_key[e], ni = sm.cq_row[e];
-    unsigned long long ck = p[0], ci = p[1];  // may be torn: the CAS validates
-    while (nk > ck || (nk == ck && ni < ci)) {
-      unsigned long long ok, oi;
-      cas128(p, ck, ci, nk, ni, ok, oi);
-      if (ok == ck && oi == ci) break;
-      ck = ok;
-      ci = oi;
+  // every loop runs a warp-uniform trip count (lane 0's count, votes): a
+  // divergent exit from this call would make the compiler guard every
+  // shuffle and vote of the sweep with divergence checks
+  const int nq = __shfl_sync(0xffffffffu, sm.cq_n, 0);
+  for (int base = 0; base < nq; base += 32) {
+    const int e = base + lane;
+    bool pend = e < nq;
+    unsigned long long* p = ccand;
+    unsigned long long nk = 0, ni = 0, ck = 0, ci = 0;
+    if (pend) {
+      p = ccand + 2 * (long long)sm.cq_col[e];
+      nk = sm.cq_key[e];
+      ni = sm.cq_row[e];
+      ck = p[0];  // may be torn: the CAS validates
+      ci = p[1];
+      pend = nk > ck || (nk == ck && ni < ci);
+    }
+    while (__any_sync(0xffffffffu, pend)) {
+      if (pend) {
+        unsigned long long ok, oi;
+        cas128(p, ck, ci, nk, ni, ok, oi);
+        if (ok == ck && oi == ci) {
+          pend = false;
+        } else {
+          ck = ok;
+          ci = oi;
+          pend = nk > ck || (nk == ck && ni < ci);
+        }
+      }
     }
   }
   __syncwarp();
@@ -691,7 +718,7 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   // make it resident, retire edge block c-2, start loading chunk c+1 (3-deep
   // rings keep the in-use slots intact)
   auto chunk_turn = [&](int c) {
-    if (SYM && sm.cq_n) col_flush(sm, lane, ccand);
+    if (SYM && __any_sync(0xffffffffu, sm.cq_n != 0)) col_flush(sm, lane, ccand);
     __syncwarp();
     if (c >= 2 && cx.write_out) {
       flush_block(sm, cx, lane, c - 2);
@@ -726,7 +753,7 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
   }
   cp_wait<0>();
   __syncwarp();
-  if (SYM && sm.cq_n) col_flush(sm, lane, ccand);
+  if (SYM && __any_sync(0xffffffffu, sm.cq_n != 0)) col_flush(sm, lane, ccand);
 #ifdef TSD_COUNT_EXACT
   if (lane == 0) atomicAdd(&g_step_count, (unsigned long long)n);
   if (lane == 0 && cx.first_seg) atomicAdd(&g_step_first, (unsigned long long)n);
@@ -1008,10 +1035,13 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
       if (lane == 0) task = atomicAdd(a.task_next, 1);
       task = __shfl_sync(0xffffffffu, task, 0);
       if (task >= a.ntasks) break;
-      const int4 t4 = a.tasks[task];
-      b0 = t4.x;
-      b1 = t4.y;
-      g = t4.z;
+      // broadcast from lane 0: provably warp-uniform, so the sweep below needs
+      // no divergence checks at its shuffles and votes
+      int4 t4 = make_int4(0, 0, 0, 0);
+      if (lane == 0) t4 = a.tasks[task];
+      b0 = __shfl_sync(0xffffffffu, t4.x, 0);
+      b1 = __shfl_sync(0xffffffffu, t4.y, 0);
+      g = __shfl_sync(0xffffffffu, t4.z, 0);
     } else {
       // dynamic queue, group-major: the groups of one band range run in
       // different waves, so each starts from the bests published by the
@@ -1035,7 +1065,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           const bool act = i < a.nrows && a.flag_a[i] == 1;
           const double ia = act ? a.invn_a[i] : 0.0;
           sm.inva[r][lane] = ia;
-          if (act) namin = fmin(namin, 1.0 / ia);
+          if (act) namin = fmin(namin, rcp_pos(ia));
         }
       }
 #pragma unroll
@@ -1267,7 +1297,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_M
           // clamped correlation units like col_update, lowered by 2^-40, so a
           // lower-triangle candidate tying with it still passes
           if (SYM && j >= 0) {
-            const double t = kplus_d(c) * (1.0 / a.invn_a[i]) * (1.0 - 0x1p-40);
+            const double t = kplus_d(c) * rcp_pos(a.invn_a[i]) * (1.0 - 0x1p-40);
             atomicMax(reinterpret_cast<long long*>(a.cthr + i), __double_as_longlong(t));
           }
         }
