@@ -399,20 +399,22 @@ __device__ __noinline__ void col_update(WarpSmem<R>& sm, int lane, unsigned cm, 
   unsigned long long bk = 0;  // order key of the lane's best corr (0 = none)
   unsigned brow = 0xffffffffu;
   if (invb > 0.0) {
-    for (unsigned mm = cm; mm; mm &= mm - 1) {
-      const int r = __ffs(mm) - 1;
+    // all slots at once (independent load -> multiply -> select chains, no
+    // serial loop over the set bits); descending slots with >= keep the
+    // lowest row on equal keys
+#pragma unroll
+    for (int r = R - 1; r >= 0; --r) {
       const int d = col - (row0 + r);
       const double ia = sm.inva[r][lane];  // 0 for inactive rows
-      if (ia > 0.0 && (d > excl || d < -excl)) {
-        // the same rounding as the row side's clamp((cov * invn_b) * invn_a):
-        // both rows of a pair see the bitwise-identical correlation, as in the
-        // reference (one value updates both, profiles.hpp:289-296)
-        const double c = clamp_corr(sm.slide[r * 32 + lane] * invb * ia);
-        const unsigned long long k = order_key(c);
-        if (k > bk || (k == bk && (unsigned)(row0 + r) < brow)) {
-          bk = k;
-          brow = (unsigned)(row0 + r);
-        }
+      // the same rounding as the row side's clamp((cov * invn_b) * invn_a):
+      // both rows of a pair see the bitwise-identical correlation, as in the
+      // reference (one value updates both, profiles.hpp:289-296)
+      const double c = clamp_corr(sm.slide[r * 32 + lane] * invb * ia);
+      const unsigned long long k = order_key(c);
+      const bool ok = ((cm >> r) & 1u) && ia > 0.0 && (d > excl || d < -excl);
+      if (ok && k >= bk) {
+        bk = k;
+        brow = (unsigned)(row0 + r);
       }
     }
   }
