@@ -1604,6 +1604,89 @@ __global__ void k_sym_init(const unsigned long long* __restrict__ seed, const do
   cthr[j] = act ? kplus_d(lb) * (1.0 / iv) * (1.0 - 0x1p-40) : DBL_MAX;
 }
 
+// ---------------------------------------------------------------------------
+// Self-join row seeds from a coarse search (symmetric sweep): the series
+// averaged over blocks of f samples is self-joined at window m / f; the
+// coarse nearest neighbour jd of coarse row t places each full-resolution
+// row i = f t + r near column f jd + r. k_seed_cand evaluates, per coarse row,
+// the diagonals through columns f jd + delta (|delta| <= 8) of its f rows:
+// one direct centred dot product (window_dot, profiles.hpp:101-108) per
+// diagonal, then the reference's recurrence (profiles.hpp:330) down the f
+// rows. The best admissible clamped correlation of a row is a lower bound of
+// its final best (an evaluation of a real cell), given to the sweep with a
+// margin (JoinInputs::seed_corr).
+__global__ void k_downsample(const double* __restrict__ x, int64_t nd, int f, double* __restrict__ xd) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nd) return;
+  double s = 0.0;
+  for (int k = 0; k < f; ++k) s += x[t * f + k];
+  xd[t] = s / f;
+}
+
+__global__ void k_seed_cand(const double* __restrict__ x, int64_t cnt, int m, long long excl, int f,
+                            const double* __restrict__ mu, const double* __restrict__ invn,
+                            const double* __restrict__ df, const double* __restrict__ dg,
+                            const uint8_t* __restrict__ flag, const int64_t* __restrict__ cbj, int64_t ncoarse,
+                            double* __restrict__ seed) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= ncoarse) return;
+  const int64_t i0 = t * f;
+  if (i0 >= cnt) return;
+  constexpr int MAXF = 16;
+  double best[MAXF];
+#pragma unroll
+  for (int r = 0; r < MAXF; ++r) best[r] = -2.0;
+  // anchors: the coarse neighbours of rows t - 1, t, t + 1 (as diagonals
+  // j - i = f (jd - a) + delta; repeated diagonals are skipped)
+  int64_t seen[3];
+  int ns = 0;
+  for (int da = -1; da <= 1; ++da) {
+    const int64_t a = t + da;
+    if (a < 0 || a >= ncoarse) continue;
+    const int64_t jd = cbj[a];
+    if (jd < 0) continue;
+    const int64_t off = f * (jd - a);
+    bool dup = false;
+    for (int q = 0; q < ns; ++q) dup |= seen[q] == off;
+    if (dup) continue;
+    seen[ns++] = off;
+    const int64_t j0 = i0 + off + (lane - 16);  // delta in [-16, 15]
+    const bool on = j0 >= 0 && j0 < cnt;
+    double cov = 0.0;
+    if (on) {
+      const double ma = mu[i0], mb = mu[j0];
+      for (int k = 0; k < m; ++k) cov = __fma_rn(x[i0 + k] - ma, x[j0 + k] - mb, cov);
+    }
+#pragma unroll
+    for (int r = 0; r < MAXF; ++r) {
+      if (r >= f) break;
+      const int64_t i = i0 + r, j = j0 + r;
+      if (on && i < cnt && j < cnt) {
+        if (r > 0) cov += __fma_rn(df[i], dg[j], dg[i] * df[j]);  // profiles.hpp:330
+        const long long d = (long long)(i - j);
+        if ((d > excl || d < -excl) && flag[i] == 1 && flag[j] == 1 && invn[i] > 0.0 && invn[j] > 0.0)
+          best[r] = fmax(best[r], clamp_corr(cov * invn[i] * invn[j]));
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < MAXF; ++r) {
+    if (r >= f) break;
+    double c = best[r];
+    for (int o = 16; o; o >>= 1) c = fmax(c, __shfl_xor_sync(0xffffffffu, c, o));
+    if (lane == 0 && i0 + r < cnt) seed[i0 + r] = c;
+  }
+}
+
+// rows that had a seed but ended without any candidate: the seed was above
+// the sweep's own value of every admissible cell (count in *bad)
+__global__ void k_seed_check(const double* __restrict__ seed, const int64_t* __restrict__ bj, int64_t n,
+                             unsigned* __restrict__ bad) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && seed[i] > -1.5 && bj[i] < 0) atomicAdd(bad, 1u);
+}
+
 template <int R, bool SELF, bool F32, bool SYM>
 int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& arena, cudaStream_t st, Error* err,
                 int* launches) {
@@ -2130,6 +2213,58 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     const char* e = getenv("TSD_SYM");
     const bool sym = in.force_sym || (e ? atoi(e) != 0 : in.rows.nwin >= 450000);
     if (!sym) return launch_join<8, true, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
+    const char* pe = getenv("TSD_SYM_SEEDS");
+    const int f = std::min(16, in.m / 32);
+    if ((pe ? atoi(pe) == 0 : false) || f < 4 || in.seed_corr || in.nshards > 1)
+      return launch_join<8, true, false, true>(in, d_best_c, d_best_j, arena, st, err, launches);
+    // coarse search for row seeds (k_seed_cand), then the symmetric sweep
+    // from them; rows a seed left empty (its margin undercut by the sweep's
+    // own rounding, never seen) send the join back through unseeded
+    const int64_t n = in.na, cnt = in.rows.nwin;
+    const int64_t nd = n / f;
+    const int md = in.m / f;
+    JoinInputs cin;
+    double* d_xd = (double*)arena.get(sizeof(double) * (nd + 64));
+    double* d_seed = (double*)arena.get(sizeof(double) * (cnt + 64));
+    unsigned* d_bad = (unsigned*)arena.get(sizeof(unsigned));
+    if (!d_xd || !d_seed || !d_bad) {
+      if (err) *err = Error{kCudaError, "device allocation failed for the self-join seeds"};
+      return kCudaError;
+    }
+    k_downsample<<<(unsigned)((nd + 255) / 256), 256, 0, st>>>(in.xa, nd, f, d_xd);
+    std::vector<Group> gd{Group{0, nd - md + 1, 0, 0}};
+    int bad_series = -1;
+    if (int rc = compute_windows(d_xd, nd, md, gd, 1, cin.rows, arena, st, &bad_series, err)) return rc;
+    cin.xa = cin.xb = d_xd;
+    cin.na = cin.nb = nd;
+    cin.cols = cin.rows;
+    cin.segs = {SegDev{0, 0, (int32_t)(nd - md + 1), 0}};
+    cin.m = md;
+    cin.excl = (in.excl + f - 1) / f;
+    cin.precision = 0;
+    const int64_t ncoarse = nd - md + 1;
+    double* d_cbc = (double*)arena.get(sizeof(double) * ncoarse);
+    int64_t* d_cbj = (int64_t*)arena.get(sizeof(int64_t) * ncoarse);
+    if (!d_cbc || !d_cbj) {
+      if (err) *err = Error{kCudaError, "device allocation failed for the self-join seeds"};
+      return kCudaError;
+    }
+    if (int rc = launch_join<8, true, false, false>(cin, d_cbc, d_cbj, arena, st, err, launches)) return rc;
+    k_seed_cand<<<(unsigned)((ncoarse * 32 + 255) / 256), 256, 0, st>>>(in.xa, cnt, in.m, in.excl, f, in.rows.mu,
+                                                                        in.rows.invn, in.rows.df, in.rows.dg,
+                                                                        in.rows.flag, d_cbj, ncoarse, d_seed);
+    if (launches) *launches += 2 + 5;
+    JoinInputs sin = in;
+    sin.seed_corr = d_seed;
+    sin.seed_margin = 1e-8;
+    if (int rc = launch_join<8, true, false, true>(sin, d_best_c, d_best_j, arena, st, err, launches)) return rc;
+    CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), st));
+    k_seed_check<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(d_seed, d_best_j, cnt, d_bad);
+    unsigned bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (getenv("TSD_VERBOSE")) fprintf(stderr, "[tsd] self-join seeds: coarse f=%d, %u rows left empty\n", f, bad);
+    if (bad == 0) return kOk;
     return launch_join<8, true, false, true>(in, d_best_c, d_best_j, arena, st, err, launches);
   }
   return launch_join<8, false, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
