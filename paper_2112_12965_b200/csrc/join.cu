@@ -1633,7 +1633,7 @@ __global__ void k_seed_cand(const double* __restrict__ x, int64_t cnt, int m, lo
   if (t >= ncoarse) return;
   const int64_t i0 = t * f;
   if (i0 >= cnt) return;
-  constexpr int MAXF = 16;
+  constexpr int MAXF = 32;
   double best[MAXF];
 #pragma unroll
   for (int r = 0; r < MAXF; ++r) best[r] = -2.0;
@@ -2212,14 +2212,21 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     // TSD_SYM=1 / 0 forces either.
     const char* e = getenv("TSD_SYM");
     const bool sym = in.force_sym || (e ? atoi(e) != 0 : in.rows.nwin >= 450000);
-    if (!sym) return launch_join<8, true, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
-    const char* pe = getenv("TSD_SYM_SEEDS");
-    const int f = std::min(16, in.m / 32);
-    if ((pe ? atoi(pe) == 0 : false) || f < 4 || in.seed_corr || in.nshards > 1)
-      return launch_join<8, true, false, true>(in, d_best_c, d_best_j, arena, st, err, launches);
-    // coarse search for row seeds (k_seed_cand), then the symmetric sweep
-    // from them; rows a seed left empty (its margin undercut by the sweep's
-    // own rounding, never seen) send the join back through unseeded
+    auto sweep = [&](const JoinInputs& x) {
+      return sym ? launch_join<8, true, false, true>(x, d_best_c, d_best_j, arena, st, err, launches)
+                 : launch_join<8, true, false, false>(x, d_best_c, d_best_j, arena, st, err, launches);
+    };
+    const char* pe = getenv("TSD_SELF_SEEDS");
+    const char* fe = getenv("TSD_SEED_F");  // development override of the coarse factor
+    const int f = fe ? std::max(4, std::min(32, atoi(fe))) : std::min(32, in.m / 16);
+    // (the symmetric sweep only: below ~450k windows, where the full-matrix
+    // sweep runs, the pre-pass costs more than it saves -- C2 6.9 -> 8.2 ms)
+    if (!sym || (pe ? atoi(pe) == 0 : false) || f < 4 || in.seed_corr || in.nshards > 1 ||
+        in.na / f < 4 * (in.m / f))
+      return sweep(in);
+    // coarse search for row seeds (k_seed_cand), then the sweep from them;
+    // rows a seed left empty (its margin undercut by the sweep's own
+    // rounding, never seen) send the join back through unseeded
     const int64_t n = in.na, cnt = in.rows.nwin;
     const int64_t nd = n / f;
     const int md = in.m / f;
@@ -2257,7 +2264,7 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     JoinInputs sin = in;
     sin.seed_corr = d_seed;
     sin.seed_margin = 1e-8;
-    if (int rc = launch_join<8, true, false, true>(sin, d_best_c, d_best_j, arena, st, err, launches)) return rc;
+    if (int rc = sweep(sin)) return rc;
     CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), st));
     k_seed_check<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(d_seed, d_best_j, cnt, d_bad);
     unsigned bad = 0;
@@ -2265,7 +2272,7 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     CUDA_TRY(cudaStreamSynchronize(st));
     if (getenv("TSD_VERBOSE")) fprintf(stderr, "[tsd] self-join seeds: coarse f=%d, %u rows left empty\n", f, bad);
     if (bad == 0) return kOk;
-    return launch_join<8, true, false, true>(in, d_best_c, d_best_j, arena, st, err, launches);
+    return sweep(in);
   }
   return launch_join<8, false, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
 }
