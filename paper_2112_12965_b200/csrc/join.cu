@@ -2263,7 +2263,8 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     if (launches) *launches += 2 + 5;
     JoinInputs sin = in;
     sin.seed_corr = d_seed;
-    sin.seed_margin = 1e-8;
+    const char* me = getenv("TSD_SEED_MARGIN");  // test hook: a negative margin forces the re-run guard
+    sin.seed_margin = me ? atof(me) : 1e-8;
     if (int rc = sweep(sin)) return rc;
     CUDA_TRY(cudaMemsetAsync(d_bad, 0, sizeof(unsigned), st));
     k_seed_check<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(d_seed, d_best_j, cnt, d_bad);

@@ -192,6 +192,26 @@ def test_symmetric_self_join_deterministic_and_equal_to_full(monkeypatch):
                   label="sym vs full")
 
 
+@pytest.mark.parametrize("margin", [None, "-0.5"])
+def test_self_join_coarse_seeds_exact_and_guarded(monkeypatch, margin):
+    """The symmetric sweep's coarse-search row seeds (k_seed_cand) only
+    filter: the profile is bit-identical to the unseeded sweep, and the oracle
+    agrees. A negative margin puts every seed above its row's best; the rows
+    left empty must send the join back through the unseeded sweep."""
+    x = synth.walk(91, 40000)
+    m = 128  # coarse factor m / 16 = 8
+    monkeypatch.setenv("TSD_SYM", "1")
+    monkeypatch.setenv("TSD_SELF_SEEDS", "0")
+    ref = tsd.self_join(x, m)
+    monkeypatch.setenv("TSD_SELF_SEEDS", "1")
+    if margin is not None:
+        monkeypatch.setenv("TSD_SEED_MARGIN", margin)
+    P = tsd.self_join(x, m)
+    assert np.array_equal(P.values, ref.values) and np.array_equal(P.indices, ref.indices)
+    rv, ri = O.self_join(x, m, m // 2)
+    check_profile(P.values, P.indices, rv, ri, m, ab_dist(x, x, m), label=f"seeded self margin={margin}")
+
+
 def test_flat_windows_ab_and_self():
     """flat stretches in query and target (profiles.hpp:290-294, :331-336)"""
     a = synth.Rng(9).noise(2000)
