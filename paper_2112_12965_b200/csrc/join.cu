@@ -1709,7 +1709,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   {
     int64_t tot = 0;
     for (const auto& s : in.segs) tot += s.ncol;
-    const int64_t lmax = std::max<int64_t>(8192, (tot + 63) / 64);
+    const char* pe = getenv("TSD_PIECE_MIN");  // development override
+    const int64_t lmax = std::max<int64_t>(pe ? atoll(pe) : 2048, (tot + 63) / 64);
     for (const auto& s : in.segs) {
       const int64_t np = (s.ncol + lmax - 1) / lmax;
       if (np <= 1) {
@@ -1744,11 +1745,13 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   // Tasks are handed out dynamically, group-major: several waves cost the
   // total over all warps plus half a task (the tail); a single wave costs one
   // task over the fraction of warps it fills (the SMs are issue-bound, and its
-  // slowest task sets the end) plus 8 %: uneven progress across SMs is not
-  // rebalanced, and no group starts from the bests an earlier group published.
-  // G > 1 costs a merge pass (16 B per row and group). At most 32 groups and
-  // 16 waves. Calibrated on C4 (G = 16, 28 bands per task: 633 -> 588 ms)
-  // and C2: profiles/README.md.
+  // slowest task sets the end) plus 25 %: uneven progress across SMs is not
+  // rebalanced, and no group starts from the bests an earlier group
+  // published (C4, random walks: 8 %; C2, ECG with many record updates:
+  // 33 %). G > 1 costs a merge pass (16 B per row and group). At most 64
+  // groups and 16 waves. Calibrated on C4 (G = 16, 28 bands per task:
+  // 633 -> 588 ms) and C2 (64 pieces of 2048 columns, one band per task:
+  // 6.9 -> 6.3 ms): profiles/README.md.
   vmark("occupancy");
   int64_t total_cols = 0;
   for (const auto& s : segs) total_cols += s.ncol;
@@ -1768,7 +1771,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   {
     double best = 1e300;
     std::vector<int> gs;
-    for (int g = 1; g <= nseg && g <= 32; g *= 2) {
+    for (int g = 1; g <= nseg && g <= 64; g *= 2) {
       split(g, gs);
       int64_t cmax = 0, smax = 0;
       for (int q = 0; q < g; ++q) {
@@ -1788,7 +1791,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
         const int64_t nt = (int64_t)((nbands + b - 1) / b) * g;
         if (nt > 16 * (int64_t)nwarps) continue;
         const double tc = b * band + top;
-        const double run = nt <= nwarps ? 1.08 * tc * nwarps / (double)nt : (double)nt * tc / nwarps + 0.5 * tc;
+        const double run = nt <= nwarps ? 1.25 * tc * nwarps / (double)nt : (double)nt * tc / nwarps + 0.5 * tc;
         const double cost = run + (g > 1 ? 30.0 * (double)nrows * g / nwarps : 0.0);
         if (cost < best * 0.999) {
           best = cost;
