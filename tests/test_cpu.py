@@ -192,3 +192,19 @@ def test_sharded_self_join_exchange_two_ranks_gloo():
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "SELFSHARD_OK" in r.stdout
+
+
+def test_file_formats_match_reference_goldens():
+    """the drop-in file formats (include/tsdict/io.hpp)
+    against the unmodified reference's (tests/golden/io_golden.tsv, made by
+    tests/golden/make_io_golden.sh): every parser case gives the reference's
+    error code or the same values bit for bit; series, profile, label and
+    dictionary text byte-identical; a dictionary written by the drop-in reads
+    back identically in the reference. Host code, no GPU."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run(["make", "-C", os.path.join(root, "tests", "cpp"), "build/test_io"], check=True,
+                   capture_output=True)
+    r = subprocess.run([os.path.join(root, "tests", "cpp", "build", "test_io"),
+                        os.path.join(root, "tests", "golden", "io_golden.tsv")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "checks match the reference" in r.stdout
