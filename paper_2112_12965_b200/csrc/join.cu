@@ -46,6 +46,10 @@ namespace tsd {
 
 namespace {
 
+#ifndef TSD_TB
+#define TSD_TB 8
+#endif
+constexpr int TB = TSD_TB;  // threshold block (columns); nmin spans TB columns (k_pack_cols)
 constexpr int WARPS = 2;  // warps per CTA (independent; small CTAs give finer occupancy steps)
 constexpr int T = 64;     // head / top-edge staging chunk (samples)
 #ifndef TSD_JOIN_MINB
@@ -330,9 +334,12 @@ __device__ __forceinline__ void issue_chunk(WarpSmem<R>& sm, const SweepCtx& cx,
 // 4-column blocks (one lane per block)
 template <int R>
 __device__ __forceinline__ void fold_cmin(WarpSmem<R>& sm, int lane, int c) {
-  if (lane < 8) {
-    const double* t = &sm.cring[(c % 3) * 32 + 4 * lane];
-    sm.cminb[(c % 3) * 8 + lane] = fmin(fmin(t[0], t[1]), fmin(t[2], t[3]));
+  if (lane < 32 / TB) {
+    const double* t = &sm.cring[(c % 3) * 32 + TB * lane];
+    double v = t[0];
+#pragma unroll
+    for (int q = 1; q < TB; ++q) v = fmin(v, t[q]);
+    sm.cminb[(c % 3) * (32 / TB) + lane] = v;
   }
   __syncwarp();
 }
@@ -521,10 +528,6 @@ __device__ __noinline__ unsigned exact_update_sym(WarpSmem<R>& sm, int lane, int
 // (thr = hi(inf), never passed by a finite cov). A pass runs the exact update
 // K = cov * invn_b > bestK against the real bestK in shared memory.
 __device__ __forceinline__ double kplus(double bK) { return bK > 0.0 ? bK : -0.0; }
-#ifndef TSD_TB
-#define TSD_TB 4
-#endif
-constexpr int TB = TSD_TB;  // threshold block (columns); nmin spans TB columns (k_pack_cols)
 
 // Column data of one step (k_pack_cols: {df_b, dg_b, invn_b, nmin}), the
 // incoming diagonal of lane 0 (edge ring) and of lanes 1..31 (shuffle)
@@ -635,8 +638,7 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
 #else
       if (SYM) {  // column side folded in: the block's weakest column threshold
 #endif
-        static_assert(TB == 4, "cminb folds 4-column blocks");
-        tcb = __double2hiint(sm.cminb[(ebase + u) >> 2] * cx.namin);
+        tcb = __double2hiint(sm.cminb[(ebase + u) / TB] * cx.namin);
       }
 #pragma unroll
       for (int r = 0; r < R; ++r) S.thr[r] = SYM ? min(__double2hiint(S.bKp[r] * nmin), tcb)
