@@ -26,6 +26,8 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
+#include <algorithm>
 
 #include "tsd_common.cuh"
 #include "tsd_internal.h"
@@ -384,7 +386,10 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
   a.seed = d_seed;
   a.excl = excl;
   a.sym = sym;
-  a.ppc = 16;
+  {
+    const char* e = getenv("TSD_HEADS_PPC");  // development override
+    a.ppc = e ? std::max(1, atoi(e)) : 16;
+  }
   if (d_seed) CUDA_TRY(cudaMemsetAsync(d_seed, 0, sizeof(unsigned long long) * nrows, st));
   const int64_t nblk = (hrows + a.Q - 1) / a.Q;
   dim3 grid((unsigned)nblk, (unsigned)((npairs + a.ppc - 1) / a.ppc));
