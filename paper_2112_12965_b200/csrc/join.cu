@@ -58,6 +58,9 @@ constexpr int T = 64;     // head / top-edge staging chunk (samples)
 #ifndef TSD_JOIN_MINB32
 #define TSD_JOIN_MINB32 8
 #endif
+#ifndef TSD_JOIN_MINB_SYM
+#define TSD_JOIN_MINB_SYM 7  // the symmetric sweep's column side wants ~146 registers (7 CTAs: 2^21 self-join -2.6 %)
+#endif
 
 template <int R>
 __host__ __device__ constexpr int padidx(int i) {
@@ -1018,7 +1021,7 @@ __device__ void sweep_segment32(WarpSmem<R32>& sm, const SweepCtx& cx, int lane,
 }
 
 template <int R, bool SELF, bool F32, bool SYM>
-__global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : TSD_JOIN_MINB) k_join(const JoinArgs a) {
+__global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_JOIN_MINB_SYM : TSD_JOIN_MINB) k_join(const JoinArgs a) {
   static_assert(!SYM || (SELF && !F32), "the symmetric sweep is the FP64 self-join");
   constexpr int H = Geo<R>::H;
   extern __shared__ __align__(16) unsigned char smem_raw[];
