@@ -56,7 +56,7 @@ constexpr int T = 64;     // head / top-edge staging chunk (samples)
 #define TSD_JOIN_MINB 8  // 8 CTAs x 2 warps per SM: caps registers at 128
 #endif
 #ifndef TSD_JOIN_MINB32
-#define TSD_JOIN_MINB32 8
+#define TSD_JOIN_MINB32 7  // 7 CTAs: more registers for the 16-row FP32 lanes (C4 FP32 kernel 402 -> 388 ms)
 #endif
 #ifndef TSD_JOIN_MINB_SYM
 #define TSD_JOIN_MINB_SYM 7  // the symmetric sweep's column side wants ~146 registers (7 CTAs: 2^21 self-join -2.6 %)
