@@ -386,12 +386,19 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
   a.seed = d_seed;
   a.excl = excl;
   a.sym = sym;
+  const int64_t nblk = (hrows + a.Q - 1) / a.Q;
   {
+    // up to 64 pairs per CTA (one forward transform per 64 inverse ones),
+    // fewer while that would leave fewer than two CTAs per SM
     const char* e = getenv("TSD_HEADS_PPC");  // development override
-    a.ppc = e ? std::max(1, atoi(e)) : 16;
+    int nsm = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    int ppc = 64;
+    while (ppc > 1 && nblk * ((npairs + ppc - 1) / ppc) < 2 * nsm) ppc >>= 1;
+    a.ppc = e ? std::max(1, atoi(e)) : ppc;
   }
   if (d_seed) CUDA_TRY(cudaMemsetAsync(d_seed, 0, sizeof(unsigned long long) * nrows, st));
-  const int64_t nblk = (hrows + a.Q - 1) / a.Q;
   dim3 grid((unsigned)nblk, (unsigned)((npairs + a.ppc - 1) / a.ppc));
   k_heads_fft<<<grid, FFT_T, smem_h, st>>>(a);
   CUDA_TRY(cudaGetLastError());

@@ -1990,9 +1990,9 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   {
     const char* e = getenv("TSD_FFT_HEADS");
     const bool want = (e ? atoi(e) != 0 : true) && nseg >= 2 && heads_fft_supported(m);
-    size_t fr = 0, tot = 0;
+    size_t fr = 0;
     const size_t hbytes = sizeof(double) * (size_t)nseg * (size_t)hstride;
-    if (want && cudaMemGetInfo(&fr, &tot) == cudaSuccess && hbytes < fr / 2) {
+    if (want && device_free_bytes(&fr) && hbytes < fr / 2) {
       d_heads = (double*)arena.get(hbytes);
       d_seed = (unsigned long long*)arena.get(sizeof(unsigned long long) * nrows);
       if (d_heads && d_seed) {
@@ -2015,10 +2015,10 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     const char* e = getenv("TSD_FFT_TOP");
     const int nbr_t = (nbands + bpt - 1) / bpt;
     tstride = (in.cols.nwin + 1) & ~int64_t(1);
-    size_t fr = 0, tot = 0;
+    size_t fr = 0;
     const size_t tbytes = sizeof(double) * (size_t)nbr_t * (size_t)tstride;
     if ((e ? atoi(e) != 0 : true) && heads_fft_supported(m) && nbr_t >= 2 &&
-        cudaMemGetInfo(&fr, &tot) == cudaSuccess && tbytes < fr / 4) {
+        device_free_bytes(&fr) && tbytes < fr / 4) {
       double* d_tw = (double*)arena.get(sizeof(double) * (size_t)nbr_t * m);
       double* d_tew = (double*)arena.get(sizeof(double) * nbr_t);
       d_te = (double*)arena.get(tbytes);
@@ -2035,8 +2035,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     }
   }
   if (getenv("TSD_VERBOSE")) {
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
+    size_t fr = 0;
+    device_free_bytes(&fr);
     fprintf(stderr, "[tsd] heads %s, top edges %s, free %.1f GB\n", d_heads ? "fft" : "in-kernel",
             d_te ? "fft" : "in-kernel", fr / 1e9);
   }

@@ -16,6 +16,7 @@
 //   k_scan_blocks   exclusive scan of the block sums (one CTA)
 //   k_scan_apply    writes P1 = prefix(x), P2 = prefix(x^2) as double-double
 //   k_window_stats  mean, std, invn, flat, df, dg per window
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 
@@ -291,8 +292,28 @@ int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group
   return kOk;
 }
 
+static std::atomic<unsigned> g_arena_gen{1};  // bumped by every arena cudaMalloc / cudaFree
+
 Arena::~Arena() {
   for (auto& b : blks) cudaFree(b.p);
+  if (!blks.empty()) g_arena_gen.fetch_add(1);
+}
+
+bool device_free_bytes(size_t* free_bytes) {
+  static thread_local unsigned gen = 0;
+  static thread_local int dev_seen = -1;
+  static thread_local size_t fr = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned g = g_arena_gen.load();
+  if (g != gen || dev != dev_seen) {
+    size_t tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return false;
+    gen = g;
+    dev_seen = dev;
+  }
+  *free_bytes = fr;
+  return true;
 }
 
 void* Arena::get(size_t bytes) {
@@ -313,6 +334,7 @@ void* Arena::get(size_t bytes) {
     cudaGetLastError();
     return nullptr;
   }
+  g_arena_gen.fetch_add(1);
   blks.push_back(Blk{(char*)p, cap, bytes});
   cur = blks.size() - 1;
   return p;

@@ -82,6 +82,14 @@ struct Arena {
   void* get(size_t bytes);  // nullptr on allocation failure
 };
 
+// Free device memory for sizing decisions (heads, top-edge tables). A real
+// cudaMemGetInfo is repeated only after some Arena has allocated or freed
+// device memory since the last one: the query itself can stall for tens of
+// milliseconds (measured up to 60 ms on B200), between the launches of a step.
+// Allocations by others are not seen; a stale estimate only makes an
+// arena.get fail, which every caller handles with its fallback.
+bool device_free_bytes(size_t* free_bytes);
+
 // stats.cu -------------------------------------------------------------------
 // Computes window arrays for the concatenated buffer d_x[0..n). `bad_series`
 // receives (host) the lowest series index holding a non-finite sample, or -1.
