@@ -691,9 +691,17 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
         // stage the slot values in slot order for the shared exact update;
         // the thresholds of raised bests are refreshed at the next threshold
         // block (stale ones only let more cells through to the exact test)
+        // the high-word test passes whole 8-column threshold blocks at once;
+        // the exact K against the register bests (possibly stale, so lower:
+        // conservative) first, the shared update only if some slot may rise
+        bool may = false;
 #pragma unroll
-        for (int r = 0; r < R; ++r) sm.slide[r * 32 + lane] = S.P[(r + ph) & (R - 1)];
-        S.dirty |= exact_update64<R, SELF>(sm, lane, col, invb, cx.row0, cx.excl);
+        for (int r = 0; r < R; ++r) may |= S.P[(r + ph) & (R - 1)] * invb > S.bKp[r] || !(S.bKp[r] > 0.0);
+        if (__any_sync(0xffffffffu, may)) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) sm.slide[r * 32 + lane] = S.P[(r + ph) & (R - 1)];
+          S.dirty |= exact_update64<R, SELF>(sm, lane, col, invb, cx.row0, cx.excl);
+        }
       }
     }
   }
