@@ -192,13 +192,19 @@ def test_symmetric_self_join_deterministic_and_equal_to_full(monkeypatch):
                   label="sym vs full")
 
 
-@pytest.mark.parametrize("margin", [None, "-0.5"])
-def test_self_join_coarse_seeds_exact_and_guarded(monkeypatch, margin):
+@pytest.mark.parametrize("margin,kind", [(None, "walk"), ("-0.5", "walk"), (None, "ecg_flat")])
+def test_self_join_coarse_seeds_exact_and_guarded(monkeypatch, margin, kind):
     """The symmetric sweep's coarse-search row seeds (k_seed_cand) only
     filter: the profile is bit-identical to the unseeded sweep, and the oracle
     agrees. A negative margin puts every seed above its row's best; the rows
     left empty must send the join back through the unseeded sweep."""
-    x = synth.walk(91, 40000)
+    if kind == "walk":
+        x = synth.walk(91, 40000)
+    else:  # quasi-periodic with flat stretches (flat rows, flat columns, exact repeats)
+        x = synth.ecg(93, 40000)[0]
+        x[5000:6500] = 0.25
+        x[21000:21400] = -1.0
+        x[30000:30300] = x[10000:10300]
     m = 128  # coarse factor m / 16 = 8
     monkeypatch.setenv("TSD_SYM", "1")
     monkeypatch.setenv("TSD_SELF_SEEDS", "0")
