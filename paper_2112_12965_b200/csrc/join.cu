@@ -1861,8 +1861,17 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       P[0] = 0.0;
       for (int b = 0; b < nbands; ++b) P[b + 1] = P[b] + (double)H * 2.5 * (double)(segs[g].ncol - qoff(b, g));
     }
+    struct PlanOpt {
+      double mk;
+      int bp;
+      std::vector<std::pair<double, int4>> cand;
+    };
+    std::vector<PlanOpt> plans;  // in increasing bands per task
     const int bpmax = std::min(nbands, 1024);
+    const char* bpe = getenv("TSD_SYM_BP");  // development override of the bands per task
+    const int bpforce = bpe ? atoi(bpe) : 0;
     for (int bp = 1; bp <= bpmax; bp *= 2) {
+      if (bpforce > 0 && bp != bpforce) continue;
       // very fine splits only add per-task overhead (top edge, head) once
       // there are many tasks per warp; skip them while a coarser one remains
       if (bp * 2 <= bpmax) {
@@ -1878,7 +1887,9 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
           const double* P = pre.data() + (size_t)g * (nbands + 1);
           double c = P[b1] - P[b0];
           if (c <= 0.0) continue;
-          c += (double)(segs[g].ncol - qoff(b0, g)) * m + (double)H * m;  // top edge + head
+          // top edge (a row of the FFT table, ~50 sweep-op units per column,
+          // or an m-term dot) + the band's left edge at an interior column
+          c += (double)(segs[g].ncol - qoff(b0, g)) * (heads_fft_supported(m) ? 50.0 : (double)m) + (double)H * m;
           cand.push_back({c, make_int4(b0, b1, g, 0)});
         }
       }
@@ -1892,15 +1903,31 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
         load.push(l);
         mk = std::max(mk, l);
       }
-      if (mk < best * 0.999) {
-        best = mk;
-        bbest = bp;
-        sym_tasks.clear();
-        // sharded (multi-GPU) self-join: every nshards-th task of the
-        // longest-first order, so each shard gets an even share of the cells
-        for (size_t q = 0; q < cand.size(); ++q)
-          if ((int)(q % (size_t)in.nshards) == in.shard) sym_tasks.push_back(cand[q].second);
-      }
+      if (getenv("TSD_VERBOSE")) fprintf(stderr, "[tsd] sym plan: %d bands per task, %zu tasks, makespan %.4g\n", bp,
+                                         cand.size(), mk);
+      plans.push_back({mk, bp, cand});
+      best = std::min(best, mk);
+    }
+    // one step finer than the estimate's best (if that estimate is within
+    // 5 %): more tasks rebalance better and let later waves start from the
+    // column bests the earlier ones raised, which the estimate does not
+    // model. Measured (ms, bands per task): 2^20 x m 256: 228 / 207 / 194
+    // for 32 / 16 / 8 (estimate 16); 2^21 x 512: 611 / 594 for 16 / 8
+    // (estimate 16); 2^22 x 512: 2362 / 2300 / 2457 for 32 / 16 / 8
+    // (estimate 32)
+    int ib = 0;
+    for (size_t q = 0; q < plans.size(); ++q)
+      if (plans[q].mk == best) ib = (int)q;
+    if (ib > 0 && plans[ib - 1].bp * 2 == plans[ib].bp && plans[ib - 1].mk <= best * 1.05) --ib;
+    for (size_t q = (size_t)ib; q < plans.size(); ++q) {
+      const PlanOpt& pl = plans[q];
+      bbest = pl.bp;
+      sym_tasks.clear();
+      // sharded (multi-GPU) self-join: every nshards-th task of the
+      // longest-first order, so each shard gets an even share of the cells
+      for (size_t q = 0; q < pl.cand.size(); ++q)
+        if ((int)(q % (size_t)in.nshards) == in.shard) sym_tasks.push_back(pl.cand[q].second);
+      break;
     }
     bpt = bbest;
     sym_cache.key = sym_key;
