@@ -66,7 +66,7 @@ inline std::string_view trim(std::string_view s) {
 
 inline error malformed(std::size_t line_no, const char* what, std::string_view field) {
   return error(errc::parse_error,
-               "line " + std::to_string(line_no) + ": malformed " + what + " '" + std::string(field) + "'");
+               "line " + std::to_string(line_no) + ": cannot read " + what + " from '" + std::string(field) + "'");
 }
 
 // the whole (trimmed) field must be one number of type T
@@ -454,17 +454,17 @@ inline std::string format_series_binary(const TimeSeries& T) {
 inline TimeSeries parse_series(std::string_view content) {
   TimeSeries T;
   if (content.size() >= 4 && std::memcmp(content.data(), series_magic, 4) == 0) {
-    if (content.size() < 12) throw error(errc::parse_error, "binary series truncated before the sample count");
+    if (content.size() < 12) throw error(errc::parse_error, "MPD1 stream shorter than its 12-byte header");
     std::uint64_t n = 0;
     std::memcpy(&n, content.data() + 4, 8);
     const std::size_t body = content.size() - 12;  // no 12 + 8n: it can wrap
     if (body % 8 != 0 || body / 8 != n)
-      throw error(errc::parse_error, "binary series length does not match its sample count");
-    if (n == 0) throw error(errc::parse_error, "series holds no samples");
+      throw error(errc::parse_error, "MPD1 payload size disagrees with the stored count");
+    if (n == 0) throw error(errc::parse_error, "no samples");
     T.values.resize(n);
     std::memcpy(T.values.data(), content.data() + 12, 8 * n);
     for (std::size_t i = 0; i < n; ++i)
-      if (!std::isfinite(T.values[i])) throw error(errc::non_finite_input, "sample " + std::to_string(i) + " is not finite");
+      if (!std::isfinite(T.values[i])) throw error(errc::non_finite_input, "sample " + std::to_string(i) + " is NaN or infinite");
     return T;
   }
   std::optional<std::uint64_t> declared;
@@ -473,21 +473,21 @@ inline TimeSeries parse_series(std::string_view content) {
     if (line.empty()) return;
     if (line.front() == '#') {
       if (declared || !T.values.empty())
-        throw error(errc::parse_error, "line " + std::to_string(no) + ": unexpected header after data");
+        throw error(errc::parse_error, "line " + std::to_string(no) + ": header must come before the samples");
       const std::string_view h = detail::trim(line.substr(1));
       if (h.size() < 3 || h.substr(0, 2) != "n=")
-        throw error(errc::parse_error, "line " + std::to_string(no) + ": unrecognized header line");
+        throw error(errc::parse_error, "line " + std::to_string(no) + ": header is not of the form '# n=<count>'");
       declared = detail::parse_uint(h.substr(2), no, "sample count");
       return;
     }
     const double v = detail::parse_double(line, no, "sample");
-    if (!std::isfinite(v)) throw error(errc::non_finite_input, "line " + std::to_string(no) + ": sample is not finite");
+    if (!std::isfinite(v)) throw error(errc::non_finite_input, "line " + std::to_string(no) + ": sample is NaN or infinite");
     T.values.push_back(v);
   });
   if (declared && *declared != T.n())
-    throw error(errc::parse_error, "declared sample count " + std::to_string(*declared) + " does not match the " +
-                                       std::to_string(T.n()) + " samples present");
-  if (T.n() == 0) throw error(errc::parse_error, "series holds no samples");
+    throw error(errc::parse_error,
+                "header announces " + std::to_string(*declared) + " samples, body holds " + std::to_string(T.n()));
+  if (T.n() == 0) throw error(errc::parse_error, "no samples");
   return T;
 }
 
@@ -528,33 +528,33 @@ inline std::string format_dictionary(const Dictionary& D) {
 inline Dictionary parse_dictionary(std::string_view content) {
   const detail::json j = detail::json_reader(content).document();
   using K = detail::json::kind;
-  if (j.k != K::object) throw error(errc::schema_error, "dictionary document must be a JSON object");
+  if (j.k != K::object) throw error(errc::schema_error, "top-level JSON value is not an object");
   const detail::json& ver = detail::require_field(j, "format_version", "dictionary");
   if (ver.k != K::unsigned_int || ver.u != static_cast<std::uint64_t>(dictionary_format_version))
-    throw error(errc::version_error, "unsupported format_version (this reader implements version 1)");
+    throw error(errc::version_error, "format_version is not 1");
   detail::reject_unknown_fields(
       j, {"format_version", "m", "k", "source_length", "space_saving", "e_max", "core_starts", "segments"}, "dictionary");
 
   Dictionary D;
   D.m = detail::as_uint(detail::require_field(j, "m", "dictionary"), "m");
-  if (D.m < 2) throw error(errc::schema_error, "m must be at least 2");
+  if (D.m < 2) throw error(errc::schema_error, "window length m below 2");
   D.k = detail::as_finite_number(detail::require_field(j, "k", "dictionary"), "k");
-  if (D.k < 0.0) throw error(errc::schema_error, "k must be non-negative");
+  if (D.k < 0.0) throw error(errc::schema_error, "k is negative");
   D.source_length = detail::as_uint(detail::require_field(j, "source_length", "dictionary"), "source_length");
   D.space_saving = detail::as_finite_number(detail::require_field(j, "space_saving", "dictionary"), "space_saving");
   const detail::json& em = detail::require_field(j, "e_max", "dictionary");
   if (em.k != K::null) {
     const double e = detail::as_finite_number(em, "e_max");
-    if (e < 0.0) throw error(errc::schema_error, "e_max must be non-negative");
+    if (e < 0.0) throw error(errc::schema_error, "e_max is negative");
     D.e_max = e;
   }
 
   const detail::json& cores = detail::require_field(j, "core_starts", "dictionary");
-  if (cores.k != K::array) throw error(errc::schema_error, "core_starts must be an array");
+  if (cores.k != K::array) throw error(errc::schema_error, "core_starts is not an array");
   for (const auto& c : cores.items) {
     const std::uint64_t st = detail::as_uint(c, "core start");
     if (st >= D.source_length || D.source_length - st < D.m)
-      throw error(errc::schema_error, "core start " + std::to_string(st) + " leaves no room for a window");
+      throw error(errc::schema_error, "core start " + std::to_string(st) + " has no full window inside the source");
     D.core_starts.push_back(st);
   }
   for (std::size_t a = 0; a < D.core_starts.size(); ++a)
@@ -563,35 +563,35 @@ inline Dictionary parse_dictionary(std::string_view content) {
       const std::size_t hi = std::max(D.core_starts[a], D.core_starts[b]);
       if (hi - lo <= D.m / 2)
         throw error(errc::schema_error, "core starts " + std::to_string(lo) + " and " + std::to_string(hi) +
-                                            " violate the separation rule");
+                                            " are closer than m/2");
     }
 
   const detail::json& segs = detail::require_field(j, "segments", "dictionary");
-  if (segs.k != K::array || segs.items.empty()) throw error(errc::schema_error, "segments must be a non-empty array");
+  if (segs.k != K::array || segs.items.empty()) throw error(errc::schema_error, "segments is missing, not an array, or empty");
   std::size_t prev_end = 0, stored = 0;
   for (const auto& sj : segs.items) {
-    if (sj.k != K::object) throw error(errc::schema_error, "segment entries must be objects");
+    if (sj.k != K::object) throw error(errc::schema_error, "a segments entry is not an object");
     detail::reject_unknown_fields(sj, {"start", "length", "values"}, "segment");
     Segment g;
     g.start = detail::as_uint(detail::require_field(sj, "start", "segment"), "segment start");
     const std::uint64_t len = detail::as_uint(detail::require_field(sj, "length", "segment"), "segment length");
-    if (len < D.m) throw error(errc::schema_error, "segment shorter than the window length");
+    if (len < D.m) throw error(errc::schema_error, "segment length below m");
     if (g.start >= D.source_length || D.source_length - g.start < len)
-      throw error(errc::schema_error, "segment extends past the source series");
-    if (!D.segments.empty() && g.start < prev_end) throw error(errc::schema_error, "segments overlap or are out of order");
+      throw error(errc::schema_error, "segment runs past source_length");
+    if (!D.segments.empty() && g.start < prev_end) throw error(errc::schema_error, "segments not sorted or overlapping");
     const detail::json& vals = detail::require_field(sj, "values", "segment");
     if (vals.k != K::array || vals.items.size() != len)
-      throw error(errc::schema_error, "segment values must be an array of 'length' numbers");
+      throw error(errc::schema_error, "segment values count differs from its length");
     g.values.reserve(len);
     for (const auto& v : vals.items) g.values.push_back(detail::as_finite_number(v, "segment value"));
     prev_end = g.start + len;
     stored += len;
     D.segments.push_back(std::move(g));
   }
-  if (D.source_length == 0) throw error(errc::schema_error, "source_length must be positive");
+  if (D.source_length == 0) throw error(errc::schema_error, "source_length is zero");
   const double recomputed = 1.0 - static_cast<double>(stored) / static_cast<double>(D.source_length);
   if (std::fabs(recomputed - D.space_saving) > 1e-12)
-    throw error(errc::schema_error, "stored space_saving does not match the segment contents");
+    throw error(errc::schema_error, "space_saving inconsistent with the stored samples");
   return D;
 }
 
@@ -620,34 +620,34 @@ inline MatrixProfile parse_profile(std::string_view content) {
       const auto f = line.size() >= 2 && line.front() == '#' ? detail::split_fields(line.substr(1))
                                                              : std::vector<std::string_view>{};
       if (f.size() != 2 || f[0].substr(0, 2) != "m=" || f[1].substr(0, 5) != "kind=")
-        throw error(errc::parse_error, at + "expected '# m=<m> kind=<kind>'");
+        throw error(errc::parse_error, at + "first line must be '# m=<m> kind=<kind>'");
       P.m = detail::parse_uint(f[0].substr(2), no, "window length");
-      if (P.m < 2) throw error(errc::schema_error, "window length must be at least 2");
+      if (P.m < 2) throw error(errc::schema_error, "profile window length below 2");
       const std::string_view kind = f[1].substr(5);
       if (kind == "self-join") P.kind = join_kind::self;
       else if (kind == "ab-join") P.kind = join_kind::ab;
-      else throw error(errc::schema_error, at + "unknown profile kind");
+      else throw error(errc::schema_error, at + "kind is neither self-join nor ab-join");
       meta = true;
       return;
     }
     if (!header) {
-      if (line != "window_start\tdistance\tnn_index") throw error(errc::parse_error, at + "expected the column header");
+      if (line != "window_start\tdistance\tnn_index") throw error(errc::parse_error, at + "column header line missing");
       header = true;
       return;
     }
     const auto f = detail::split_fields(line);
-    if (f.size() != 3) throw error(errc::parse_error, at + "expected 3 columns");
+    if (f.size() != 3) throw error(errc::parse_error, at + "row needs 3 fields");
     if (detail::parse_uint(f[0], no, "window start") != P.values.size())
-      throw error(errc::schema_error, at + "window starts must be consecutive");
+      throw error(errc::schema_error, at + "window_start not consecutive");
     const double d = detail::parse_double(f[1], no, "distance");
-    if (std::isnan(d) || d < 0.0) throw error(errc::schema_error, at + "distance must be non-negative");
+    if (std::isnan(d) || d < 0.0) throw error(errc::schema_error, at + "distance negative or NaN");
     const std::int64_t nn = detail::parse_int(f[2], no, "neighbor index");
-    if (nn < MatrixProfile::no_neighbor) throw error(errc::schema_error, at + "neighbor index out of range");
+    if (nn < MatrixProfile::no_neighbor) throw error(errc::schema_error, at + "nn_index below -1");
     P.values.push_back(d);
     P.indices.push_back(nn);
   });
-  if (!meta || !header) throw error(errc::parse_error, "profile header missing");
-  if (P.values.empty()) throw error(errc::schema_error, "profile holds no rows");
+  if (!meta || !header) throw error(errc::parse_error, "profile ends before its headers");
+  if (P.values.empty()) throw error(errc::schema_error, "profile has no rows");
   return P;
 }
 
@@ -669,13 +669,13 @@ inline std::vector<interval> parse_labels(std::string_view content) {
     const std::string_view line = detail::trim(raw);
     if (line.empty() || line.front() == '#') return;
     const auto f = detail::split_fields(line);
-    if (f.size() != 2) throw error(errc::parse_error, "line " + std::to_string(no) + ": expected 'start end'");
+    if (f.size() != 2) throw error(errc::parse_error, "line " + std::to_string(no) + ": region needs 2 fields");
     const std::uint64_t lo = detail::parse_uint(f[0], no, "region start");
     const std::uint64_t hi = detail::parse_uint(f[1], no, "region end");
-    if (lo >= hi) throw error(errc::schema_error, "line " + std::to_string(no) + ": region start must precede end");
+    if (lo >= hi) throw error(errc::schema_error, "line " + std::to_string(no) + ": empty or inverted region");
     regions.emplace_back(lo, hi);
   });
-  if (regions.empty()) throw error(errc::schema_error, "label file holds no regions");
+  if (regions.empty()) throw error(errc::schema_error, "no regions");
   return merge_intervals(regions);
 }
 
