@@ -64,14 +64,17 @@ inline std::string_view trim(std::string_view s) {
   return s.substr(a, b - a);
 }
 
+// "line N: " prefix of a text-format diagnostic
+inline std::string at_line(std::size_t no) { return "line " + std::to_string(no) + ": "; }
+
 inline error malformed(std::size_t line_no, const char* what, std::string_view field) {
   return error(errc::parse_error,
-               "line " + std::to_string(line_no) + ": cannot read " + what + " from '" + std::string(field) + "'");
+               at_line(line_no) + "cannot read " + what + " from '" + std::string(field) + "'");
 }
 
 // the whole (trimmed) field must be one number of type T
 template <class T>
-inline T parse_number(std::string_view field, std::size_t line_no, const char* what) {
+inline T whole_number(std::string_view field, std::size_t line_no, const char* what) {
   field = trim(field);
   T v{};
   const char* end = field.data() + field.size();
@@ -80,17 +83,17 @@ inline T parse_number(std::string_view field, std::size_t line_no, const char* w
   return v;
 }
 inline double parse_double(std::string_view f, std::size_t line_no, const char* what) {
-  return parse_number<double>(f, line_no, what);
+  return whole_number<double>(f, line_no, what);
 }
 inline std::uint64_t parse_uint(std::string_view f, std::size_t line_no, const char* what) {
-  return parse_number<std::uint64_t>(f, line_no, what);
+  return whole_number<std::uint64_t>(f, line_no, what);
 }
 inline std::int64_t parse_int(std::string_view f, std::size_t line_no, const char* what) {
-  return parse_number<std::int64_t>(f, line_no, what);
+  return whole_number<std::int64_t>(f, line_no, what);
 }
 
 // shortest decimal that reads back to the same double
-inline std::string format_double(double v) {
+inline std::string shortest(double v) {
   char buf[64];
   const auto r = std::to_chars(buf, buf + sizeof buf, v);
   return std::string(buf, r.ptr);
@@ -99,7 +102,7 @@ inline std::string format_double(double v) {
 // calls fn(line number from 1, line) for every '\n'-separated line; a
 // trailing newline yields one last empty line, as the reference does
 template <class F>
-inline void for_each_line(std::string_view text, F&& fn) {
+inline void each_line(std::string_view text, F&& fn) {
   std::size_t no = 1, pos = 0;
   for (;;) {
     const std::size_t nl = text.find('\n', pos);
@@ -110,7 +113,7 @@ inline void for_each_line(std::string_view text, F&& fn) {
 }
 
 // fields separated by runs of spaces, tabs or commas
-inline std::vector<std::string_view> split_fields(std::string_view line) {
+inline std::vector<std::string_view> fields_of(std::string_view line) {
   std::vector<std::string_view> out;
   auto sep = [](char c) { return c == ' ' || c == '\t' || c == ','; };
   std::size_t i = 0;
@@ -123,7 +126,7 @@ inline std::vector<std::string_view> split_fields(std::string_view line) {
   return out;
 }
 
-inline std::string slurp(const std::string& path) {
+inline std::string read_file(const std::string& path) {
   std::ifstream in(path, std::ios::binary);
   if (!in) throw error(errc::io_error, "cannot open '" + path + "' for reading");
   std::ostringstream ss;
@@ -132,7 +135,7 @@ inline std::string slurp(const std::string& path) {
   return std::move(ss).str();
 }
 
-inline void spill(const std::string& path, std::string_view content) {
+inline void write_file(const std::string& path, std::string_view content) {
   std::ofstream out(path, std::ios::binary | std::ios::trunc);
   if (!out) throw error(errc::io_error, "cannot open '" + path + "' for writing");
   out.write(content.data(), static_cast<std::streamsize>(content.size()));
@@ -368,7 +371,7 @@ class json_reader {
 // as digits with trailing zeros and ".0" when k <= n <= 15, with a decimal
 // point inside when 0 < n <= 15, as "0.000d" when -4 < n <= 0, else in
 // exponent form "d.ddde+XX" (sign always, at least two exponent digits)
-inline std::string json_double(double v) {
+inline std::string json_number(double v) {
   if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
   char buf[64];
   const auto r = std::to_chars(buf, buf + sizeof buf, v, std::chars_format::scientific);
@@ -401,7 +404,7 @@ inline std::string json_double(double v) {
   return out;
 }
 
-inline void reject_unknown_fields(const json& obj, std::initializer_list<std::string_view> known,
+inline void check_members(const json& obj, std::initializer_list<std::string_view> known,
                                   const char* where) {
   for (const auto& f : obj.fields) {
     if (std::find(known.begin(), known.end(), std::string_view(f.first)) == known.end())
@@ -410,18 +413,18 @@ inline void reject_unknown_fields(const json& obj, std::initializer_list<std::st
   }
 }
 
-inline const json& require_field(const json& obj, const char* key, const char* where) {
+inline const json& member(const json& obj, const char* key, const char* where) {
   const json* v = obj.find(key);
   if (!v) throw error(errc::schema_error, std::string("missing field '") + key + "' in " + where);
   return *v;
 }
 
-inline std::uint64_t as_uint(const json& v, const char* what) {
+inline std::uint64_t u64_of(const json& v, const char* what) {
   if (v.k != json::kind::unsigned_int) throw error(errc::schema_error, std::string(what) + " must be a non-negative integer");
   return v.u;
 }
 
-inline double as_finite_number(const json& v, const char* what) {
+inline double finite_of(const json& v, const char* what) {
   if (!v.is_number()) throw error(errc::schema_error, std::string(what) + " must be a number");
   const double d = v.as_double();
   if (!std::isfinite(d)) throw error(errc::non_finite_input, std::string(what) + " is not finite");
@@ -436,7 +439,7 @@ inline constexpr char series_magic[4] = {'M', 'P', 'D', '1'};
 
 inline std::string format_series_text(const TimeSeries& T) {
   std::string out = "# n=" + std::to_string(T.n()) + "\n";
-  for (double v : T.values) (out += detail::format_double(v)) += '\n';
+  for (double v : T.values) (out += detail::shortest(v)) += '\n';
   return out;
 }
 
@@ -468,20 +471,20 @@ inline TimeSeries parse_series(std::string_view content) {
     return T;
   }
   std::optional<std::uint64_t> declared;
-  detail::for_each_line(content, [&](std::size_t no, std::string_view raw) {
+  detail::each_line(content, [&](std::size_t no, std::string_view raw) {
     const std::string_view line = detail::trim(raw);
     if (line.empty()) return;
     if (line.front() == '#') {
       if (declared || !T.values.empty())
-        throw error(errc::parse_error, "line " + std::to_string(no) + ": header must come before the samples");
+        throw error(errc::parse_error, detail::at_line(no) + "header must come before the samples");
       const std::string_view h = detail::trim(line.substr(1));
       if (h.size() < 3 || h.substr(0, 2) != "n=")
-        throw error(errc::parse_error, "line " + std::to_string(no) + ": header is not of the form '# n=<count>'");
+        throw error(errc::parse_error, detail::at_line(no) + "header is not of the form '# n=<count>'");
       declared = detail::parse_uint(h.substr(2), no, "sample count");
       return;
     }
     const double v = detail::parse_double(line, no, "sample");
-    if (!std::isfinite(v)) throw error(errc::non_finite_input, "line " + std::to_string(no) + ": sample is NaN or infinite");
+    if (!std::isfinite(v)) throw error(errc::non_finite_input, detail::at_line(no) + "sample is NaN or infinite");
     T.values.push_back(v);
   });
   if (declared && *declared != T.n())
@@ -491,10 +494,10 @@ inline TimeSeries parse_series(std::string_view content) {
   return T;
 }
 
-inline TimeSeries read_series(const std::string& path) { return parse_series(detail::slurp(path)); }
-inline void write_series_text(const std::string& path, const TimeSeries& T) { detail::spill(path, format_series_text(T)); }
+inline TimeSeries read_series(const std::string& path) { return parse_series(detail::read_file(path)); }
+inline void write_series_text(const std::string& path, const TimeSeries& T) { detail::write_file(path, format_series_text(T)); }
 inline void write_series_binary(const std::string& path, const TimeSeries& T) {
-  detail::spill(path, format_series_binary(T));
+  detail::write_file(path, format_series_binary(T));
 }
 
 // -------------------------------------------------------------- dictionary
@@ -506,20 +509,20 @@ inline std::string format_dictionary(const Dictionary& D) {
   std::string o = "{\"core_starts\":[";
   for (std::size_t i = 0; i < D.core_starts.size(); ++i) (o += i ? "," : "") += std::to_string(D.core_starts[i]);
   o += "],\"e_max\":";
-  o += D.e_max ? detail::json_double(*D.e_max) : "null";
+  o += D.e_max ? detail::json_number(*D.e_max) : "null";
   o += ",\"format_version\":" + std::to_string(dictionary_format_version);
-  o += ",\"k\":" + detail::json_double(D.k);
+  o += ",\"k\":" + detail::json_number(D.k);
   o += ",\"m\":" + std::to_string(D.m);
   o += ",\"segments\":[";
   for (std::size_t s = 0; s < D.segments.size(); ++s) {
     const Segment& g = D.segments[s];
     o += s ? ",{" : "{";
     o += "\"length\":" + std::to_string(g.length()) + ",\"start\":" + std::to_string(g.start) + ",\"values\":[";
-    for (std::size_t i = 0; i < g.values.size(); ++i) (o += i ? "," : "") += detail::json_double(g.values[i]);
+    for (std::size_t i = 0; i < g.values.size(); ++i) (o += i ? "," : "") += detail::json_number(g.values[i]);
     o += "]}";
   }
   o += "],\"source_length\":" + std::to_string(D.source_length);
-  o += ",\"space_saving\":" + detail::json_double(D.space_saving);
+  o += ",\"space_saving\":" + detail::json_number(D.space_saving);
   o += "}\n";
   return o;
 }
@@ -529,30 +532,30 @@ inline Dictionary parse_dictionary(std::string_view content) {
   const detail::json j = detail::json_reader(content).document();
   using K = detail::json::kind;
   if (j.k != K::object) throw error(errc::schema_error, "top-level JSON value is not an object");
-  const detail::json& ver = detail::require_field(j, "format_version", "dictionary");
+  const detail::json& ver = detail::member(j, "format_version", "dictionary");
   if (ver.k != K::unsigned_int || ver.u != static_cast<std::uint64_t>(dictionary_format_version))
     throw error(errc::version_error, "format_version is not 1");
-  detail::reject_unknown_fields(
+  detail::check_members(
       j, {"format_version", "m", "k", "source_length", "space_saving", "e_max", "core_starts", "segments"}, "dictionary");
 
   Dictionary D;
-  D.m = detail::as_uint(detail::require_field(j, "m", "dictionary"), "m");
+  D.m = detail::u64_of(detail::member(j, "m", "dictionary"), "m");
   if (D.m < 2) throw error(errc::schema_error, "window length m below 2");
-  D.k = detail::as_finite_number(detail::require_field(j, "k", "dictionary"), "k");
+  D.k = detail::finite_of(detail::member(j, "k", "dictionary"), "k");
   if (D.k < 0.0) throw error(errc::schema_error, "k is negative");
-  D.source_length = detail::as_uint(detail::require_field(j, "source_length", "dictionary"), "source_length");
-  D.space_saving = detail::as_finite_number(detail::require_field(j, "space_saving", "dictionary"), "space_saving");
-  const detail::json& em = detail::require_field(j, "e_max", "dictionary");
+  D.source_length = detail::u64_of(detail::member(j, "source_length", "dictionary"), "source_length");
+  D.space_saving = detail::finite_of(detail::member(j, "space_saving", "dictionary"), "space_saving");
+  const detail::json& em = detail::member(j, "e_max", "dictionary");
   if (em.k != K::null) {
-    const double e = detail::as_finite_number(em, "e_max");
+    const double e = detail::finite_of(em, "e_max");
     if (e < 0.0) throw error(errc::schema_error, "e_max is negative");
     D.e_max = e;
   }
 
-  const detail::json& cores = detail::require_field(j, "core_starts", "dictionary");
+  const detail::json& cores = detail::member(j, "core_starts", "dictionary");
   if (cores.k != K::array) throw error(errc::schema_error, "core_starts is not an array");
   for (const auto& c : cores.items) {
-    const std::uint64_t st = detail::as_uint(c, "core start");
+    const std::uint64_t st = detail::u64_of(c, "core start");
     if (st >= D.source_length || D.source_length - st < D.m)
       throw error(errc::schema_error, "core start " + std::to_string(st) + " has no full window inside the source");
     D.core_starts.push_back(st);
@@ -566,24 +569,24 @@ inline Dictionary parse_dictionary(std::string_view content) {
                                             " are closer than m/2");
     }
 
-  const detail::json& segs = detail::require_field(j, "segments", "dictionary");
+  const detail::json& segs = detail::member(j, "segments", "dictionary");
   if (segs.k != K::array || segs.items.empty()) throw error(errc::schema_error, "segments is missing, not an array, or empty");
   std::size_t prev_end = 0, stored = 0;
   for (const auto& sj : segs.items) {
     if (sj.k != K::object) throw error(errc::schema_error, "a segments entry is not an object");
-    detail::reject_unknown_fields(sj, {"start", "length", "values"}, "segment");
+    detail::check_members(sj, {"start", "length", "values"}, "segment");
     Segment g;
-    g.start = detail::as_uint(detail::require_field(sj, "start", "segment"), "segment start");
-    const std::uint64_t len = detail::as_uint(detail::require_field(sj, "length", "segment"), "segment length");
+    g.start = detail::u64_of(detail::member(sj, "start", "segment"), "segment start");
+    const std::uint64_t len = detail::u64_of(detail::member(sj, "length", "segment"), "segment length");
     if (len < D.m) throw error(errc::schema_error, "segment length below m");
     if (g.start >= D.source_length || D.source_length - g.start < len)
       throw error(errc::schema_error, "segment runs past source_length");
     if (!D.segments.empty() && g.start < prev_end) throw error(errc::schema_error, "segments not sorted or overlapping");
-    const detail::json& vals = detail::require_field(sj, "values", "segment");
+    const detail::json& vals = detail::member(sj, "values", "segment");
     if (vals.k != K::array || vals.items.size() != len)
       throw error(errc::schema_error, "segment values count differs from its length");
     g.values.reserve(len);
-    for (const auto& v : vals.items) g.values.push_back(detail::as_finite_number(v, "segment value"));
+    for (const auto& v : vals.items) g.values.push_back(detail::finite_of(v, "segment value"));
     prev_end = g.start + len;
     stored += len;
     D.segments.push_back(std::move(g));
@@ -595,8 +598,8 @@ inline Dictionary parse_dictionary(std::string_view content) {
   return D;
 }
 
-inline Dictionary read_dictionary(const std::string& path) { return parse_dictionary(detail::slurp(path)); }
-inline void write_dictionary(const std::string& path, const Dictionary& D) { detail::spill(path, format_dictionary(D)); }
+inline Dictionary read_dictionary(const std::string& path) { return parse_dictionary(detail::read_file(path)); }
+inline void write_dictionary(const std::string& path, const Dictionary& D) { detail::write_file(path, format_dictionary(D)); }
 
 // ----------------------------------------------------------------- profile
 
@@ -605,19 +608,19 @@ inline const char* join_kind_name(join_kind k) { return k == join_kind::self ? "
 inline std::string format_profile(const MatrixProfile& P) {
   std::string o = "# m=" + std::to_string(P.m) + " kind=" + join_kind_name(P.kind) + "\nwindow_start\tdistance\tnn_index\n";
   for (std::size_t i = 0; i < P.values.size(); ++i)
-    o += std::to_string(i) + '\t' + detail::format_double(P.values[i]) + '\t' + std::to_string(P.indices[i]) + '\n';
+    o += std::to_string(i) + '\t' + detail::shortest(P.values[i]) + '\t' + std::to_string(P.indices[i]) + '\n';
   return o;
 }
 
 inline MatrixProfile parse_profile(std::string_view content) {
   MatrixProfile P;
   bool meta = false, header = false;
-  detail::for_each_line(content, [&](std::size_t no, std::string_view raw) {
+  detail::each_line(content, [&](std::size_t no, std::string_view raw) {
     const std::string_view line = detail::trim(raw);
     if (line.empty()) return;
-    const std::string at = "line " + std::to_string(no) + ": ";
+    const std::string at = detail::at_line(no) + "";
     if (!meta) {
-      const auto f = line.size() >= 2 && line.front() == '#' ? detail::split_fields(line.substr(1))
+      const auto f = line.size() >= 2 && line.front() == '#' ? detail::fields_of(line.substr(1))
                                                              : std::vector<std::string_view>{};
       if (f.size() != 2 || f[0].substr(0, 2) != "m=" || f[1].substr(0, 5) != "kind=")
         throw error(errc::parse_error, at + "first line must be '# m=<m> kind=<kind>'");
@@ -635,7 +638,7 @@ inline MatrixProfile parse_profile(std::string_view content) {
       header = true;
       return;
     }
-    const auto f = detail::split_fields(line);
+    const auto f = detail::fields_of(line);
     if (f.size() != 3) throw error(errc::parse_error, at + "row needs 3 fields");
     if (detail::parse_uint(f[0], no, "window start") != P.values.size())
       throw error(errc::schema_error, at + "window_start not consecutive");
@@ -651,8 +654,8 @@ inline MatrixProfile parse_profile(std::string_view content) {
   return P;
 }
 
-inline MatrixProfile read_profile(const std::string& path) { return parse_profile(detail::slurp(path)); }
-inline void write_profile(const std::string& path, const MatrixProfile& P) { detail::spill(path, format_profile(P)); }
+inline MatrixProfile read_profile(const std::string& path) { return parse_profile(detail::read_file(path)); }
+inline void write_profile(const std::string& path, const MatrixProfile& P) { detail::write_file(path, format_profile(P)); }
 
 // ------------------------------------------------------------------ labels
 
@@ -665,23 +668,23 @@ inline std::string format_labels(const std::vector<interval>& regions) {
 // regions come back sorted and merged (overlapping or touching ones collapse)
 inline std::vector<interval> parse_labels(std::string_view content) {
   std::vector<interval> regions;
-  detail::for_each_line(content, [&](std::size_t no, std::string_view raw) {
+  detail::each_line(content, [&](std::size_t no, std::string_view raw) {
     const std::string_view line = detail::trim(raw);
     if (line.empty() || line.front() == '#') return;
-    const auto f = detail::split_fields(line);
-    if (f.size() != 2) throw error(errc::parse_error, "line " + std::to_string(no) + ": region needs 2 fields");
+    const auto f = detail::fields_of(line);
+    if (f.size() != 2) throw error(errc::parse_error, detail::at_line(no) + "region needs 2 fields");
     const std::uint64_t lo = detail::parse_uint(f[0], no, "region start");
     const std::uint64_t hi = detail::parse_uint(f[1], no, "region end");
-    if (lo >= hi) throw error(errc::schema_error, "line " + std::to_string(no) + ": empty or inverted region");
+    if (lo >= hi) throw error(errc::schema_error, detail::at_line(no) + "empty or inverted region");
     regions.emplace_back(lo, hi);
   });
   if (regions.empty()) throw error(errc::schema_error, "no regions");
   return merge_intervals(regions);
 }
 
-inline std::vector<interval> read_labels(const std::string& path) { return parse_labels(detail::slurp(path)); }
+inline std::vector<interval> read_labels(const std::string& path) { return parse_labels(detail::read_file(path)); }
 inline void write_labels(const std::string& path, const std::vector<interval>& regions) {
-  detail::spill(path, format_labels(regions));
+  detail::write_file(path, format_labels(regions));
 }
 
 }  // namespace tsdict

@@ -49,7 +49,7 @@ static Dictionary golden_dictionary() {  // the same document as oracle/ref_io_g
 
 int main(int argc, char** argv) {
   if (argc == 3 && std::string(argv[1]) == "emit-dict") {
-    detail::spill(argv[2], format_dictionary(golden_dictionary()));
+    detail::write_file(argv[2], format_dictionary(golden_dictionary()));
     return 0;
   }
   if (argc != 2) {
