@@ -50,7 +50,10 @@ namespace {
 #define TSD_TB 8
 #endif
 constexpr int TB = TSD_TB;  // threshold block (columns); nmin spans TB columns (k_pack_cols)
-constexpr int WARPS = 2;  // warps per CTA (independent; small CTAs give finer occupancy steps)
+#ifndef TSD_WARPS
+#define TSD_WARPS 2
+#endif
+constexpr int WARPS = TSD_WARPS;  // warps per CTA (independent; small CTAs give finer occupancy steps)
 constexpr int T = 64;     // head / top-edge staging chunk (samples)
 #ifndef TSD_JOIN_MINB
 #define TSD_JOIN_MINB 8  // 8 CTAs x 2 warps per SM: caps registers at 128
