@@ -417,7 +417,8 @@ def self_join_lines(q, dist=None, world=1):
             print(f"[bench] {name}: {[round(v * 1e3, 2) for v in ts]} ms", file=sys.stderr, flush=True)
         out[name] = {"n": int(x.size), "m": m, "excl": e, "pairs": pairs, "ms": t * 1e3,
                      "value": pairs / t / 1e9, "unit": "GPair/s",
-                     "kernel": "symmetric upper-triangle sweep" if cnt >= 450000 else "full-matrix sweep"}
+                     "kernel": "symmetric upper-triangle sweep" if (m >= 192 and cnt >= max(98304, (1 << 26) // m))
+                     else "full-matrix sweep"}
     return out
 
 

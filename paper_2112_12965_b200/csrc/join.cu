@@ -2256,12 +2256,19 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
   if (self) {
     // The symmetric upper-triangle sweep evaluates each admissible pair once
     // and updates both rows, as the reference does (profiles.hpp:287-297).
-    // Its column side needs the bests of earlier waves of bands to filter
-    // well, so it wins from ~450k windows (several waves on 148 SMs); below
-    // that the full-matrix sweep (every pair from both rows) is faster.
-    // TSD_SYM=1 / 0 forces either.
+    // Its column side filters well only with distinctive windows and enough
+    // waves of bands, so it wins from about 2^26 / m windows for m >= 192;
+    // below that, and for short windows at any size, the full-matrix sweep
+    // (every pair from both rows) is faster. TSD_SYM=1 / 0 forces either.
     const char* e = getenv("TSD_SYM");
-    const bool sym = in.force_sym || (e ? atoi(e) != 0 : in.rows.nwin >= 450000);
+    // Crossover measured on walks / ECG (host API, ms full vs symmetric):
+    // m = 1024: 65k 1.9/2.8, 98k 4.0/3.7; m = 512: 65k 2.0/2.6, 131k 5.5/5.2,
+    // 2^21 ~1000/590; m = 250: 131k 6.0/7.0, 262k 19.9/19.0, 393k 42/38;
+    // m = 128: 786k 163/208; m = 64: 1M 305/833 (short windows leave the
+    // column side too many near-best candidates).
+    const bool auto_sym =
+        in.m >= 192 && in.rows.nwin >= std::max<int64_t>(98304, (int64_t(1) << 26) / std::max(1, in.m));
+    const bool sym = in.force_sym || (e ? atoi(e) != 0 : auto_sym);
     auto sweep = [&](const JoinInputs& x) {
       return sym ? launch_join<8, true, false, true>(x, d_best_c, d_best_j, arena, st, err, launches)
                  : launch_join<8, true, false, false>(x, d_best_c, d_best_j, arena, st, err, launches);
@@ -2269,7 +2276,7 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     const char* pe = getenv("TSD_SELF_SEEDS");
     const char* fe = getenv("TSD_SEED_F");  // development override of the coarse factor
     const int f = fe ? std::max(4, std::min(32, atoi(fe))) : std::min(32, in.m / 16);
-    // (the symmetric sweep only: below ~450k windows, where the full-matrix
+    // (the symmetric sweep only: at C2's size, where the full-matrix
     // sweep runs, the pre-pass costs more than it saves -- C2 6.9 -> 8.2 ms)
     if (!sym || (pe ? atoi(pe) == 0 : false) || f < 4 || in.seed_corr || in.nshards > 1 ||
         in.na / f < 4 * (in.m / f))
