@@ -2278,7 +2278,8 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     const int f = fe ? std::max(4, std::min(32, atoi(fe))) : std::min(32, in.m / 16);
     // (the symmetric sweep only: at C2's size, where the full-matrix
     // sweep runs, the pre-pass costs more than it saves -- C2 6.9 -> 8.2 ms)
-    if (!sym || (pe ? atoi(pe) == 0 : false) || f < 4 || in.seed_corr || in.nshards > 1 ||
+    const int seeds_mode = pe ? atoi(pe) : 1;  // 0 off, 1 symmetric sweep only, 2 both sweeps (experiments)
+    if ((!sym && seeds_mode < 2) || seeds_mode == 0 || f < 4 || in.seed_corr || in.nshards > 1 ||
         in.na / f < 4 * (in.m / f))
       return sweep(in);
     // coarse search for row seeds (k_seed_cand), then the sweep from them;
