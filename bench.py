@@ -11,6 +11,11 @@ synthetic data with the BASELINE shapes (no dataset needed).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
     python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
 
+The same JSON line also carries every other BASELINE config ("configs": C1,
+C2, C3, C5 and C4 in the FP32 mode; inputs from workloads.py), each with its
+device time, roofline fraction and a same-run CPU baseline of the reference
+itself, plus the self-join target shape (2^21 x m = 512).
+
 N > 1: weak scaling -- every rank joins its own C4 query (seed 4 + rank)
 against the same dictionary; no collective on the data path (rows are
 independent). Timing: CUDA events on the launching stream,
@@ -38,7 +43,7 @@ SEG_LEN = 1024
 M = 512
 Q_SEED, D_SEED = 4, 5
 FLOPS_PER_CELL = 6  # profiles.hpp:330-331: 2 mul + 2 add (update) + 2 mul (normalise)
-CPU_SAMPLE_WINDOWS = 1 << 15  # bounded CPU-baseline sample (query windows)
+CPU_SAMPLE_WINDOWS = 1 << 17  # bounded CPU-baseline sample of C4 (query windows; 2^17-2^18)
 
 
 def cells_per_step(q_len=Q_LEN):
@@ -148,6 +153,28 @@ def cpu_reference_gcells(q, segs, threads, windows=CPU_SAMPLE_WINDOWS):
     cells = windows * N_SEG * (SEG_LEN - M + 1)
     return {"value": cells / dt / 1e9, "unit": "GCell/s", "cores": cores, "kind": kind,
             "sample": f"first {windows} query windows of C4 x all 256 segments ({cells:.3e} cells, {dt:.1f} s)"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _timed(fn, reps=1):
+    """best-of-reps wall time of fn() (the reference bench's rule, tools/tsdict.cpp:219-230)"""
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best
 
 
 def run_reference(args):
@@ -274,15 +301,29 @@ def run_gpu(args):
     same = bool(torch.equal(h_idx, d_idx.cpu())) and bool(torch.equal(h_val, d_val.cpu()))
 
     plan.close()  # release the FP64 plan's device arenas before the FP32 plan
+    del h_q, h_val, h_idx
     fp32 = fp32_line(D, d_q, d_val, d_idx, stream, flush, dev, dist, world)
+    del d_q, d_val, d_idx
+    torch.cuda.empty_cache()
     sj = self_join_lines(q, dist, world)  # every rank (the sharded run needs all of them)
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return 0
-    peak = tsd.measure_peak("fp64", seconds=2.0)
+    peak_meas, peak_mhz = tsd.measure_peak_clock("fp64", seconds=2.0)
+    nominal = nominal_peaks(dev, clk.summary())
+    peak = nominal["fp64"]
     for v in sj.values():  # against the FP64 cell peak of the GPUs used
         v["frac_of_fp64_cell_peak"] = v["value"] * 1e9 / (v.get("n_gpus", 1) * peak / FLOPS_PER_CELL)
+        if v.get("kernel_ms"):
+            v["kernel_frac"] = FLOPS_PER_CELL * v["pairs"] / (v["kernel_ms"] * 1e-3) / peak
+    fp32["roofline"]["peak_measured"] = fp32["roofline"]["peak"]
+    fp32["roofline"]["peak"] = nominal["fp32"] / 1e12
+    fp32["roofline"]["frac_of_measured"] = fp32["roofline"]["frac"]
+    fp32["roofline"]["frac"] = fp32["roofline"]["achieved"] * 1e12 / nominal["fp32"]
+    fp32["roofline"]["peak_def"] = ("nominal FFMA peak: %d SMs x 128 lanes x 2 flops x %.0f MHz (max SM clock); "
+                                    "peak_measured: FFMA loop measured live" % (nominal["sms"], nominal["mhz"]))
+    configs = config_lines(args, dev, stream, flush, peak, nominal)
     jms = statistics.median(join_ms)
     kms = statistics.median(kernel_ms)
     hms = statistics.median(heads_ms)
@@ -290,6 +331,8 @@ def run_gpu(args):
     traffic = args.traffic if args.traffic is not None else committed_traffic()
     roofline = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
+                "peak_measured": peak_meas / 1e12, "frac_of_measured": achieved / peak_meas,
+                "peak_measured_sm_mhz": peak_mhz,
                 "kernel": "k_join<8,false,false> (FP64 row-band join)", "achieved_def":
                     "6 FP64 flops per valid cell (profiles.hpp:330-331) x cells per launch / median duration of "
                     "the join kernel (CUDA events around its launch, on the launching stream)",
@@ -298,9 +341,14 @@ def run_gpu(args):
                 "pipeline": {"join_ms_median": jms, "kernel_ms_median": kms, "heads_fft_ms_median": hms,
                              "frac": FLOPS_PER_CELL * cells_per_step() / (jms * 1e-3) / peak,
                              "def": "the whole join phase (column packing, FFT heads, join kernel, group merge)"},
-                "peak_def": "DFMA throughput measured live by tsd_measure_peak (2 s sustained, this GPU); "
-                            "MEASURED_PEAKS.json has no FP64 entry"}
+                "peak_def": "nominal DFMA peak: %d SMs x 64 FP64 FMA/clk x 2 flops x %.0f MHz (max SM clock; "
+                            "MEASURED_PEAKS.json has no FP64 entry); peak_measured: a DFMA loop timed live on this "
+                            "GPU for 2 s (tsd_measure_peak_clock, SM clock it ran at: peak_measured_sm_mhz)"
+                            % (nominal["sms"], nominal["mhz"])}
     cpu = cpu_reference_gcells(q, segs, os.cpu_count() or 1) if world == 1 or rank == 0 else None
+    if cpu:
+        cpu["cpu_model"] = cpu_model()
+        cpu["extrapolated"] = True
     line = {"metric": "AB-join distance cells/sec", "value": value, "unit": "GCell/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -313,6 +361,7 @@ def run_gpu(args):
             "gpu_launches": launches, "clocks": clk.summary(),
             "fp32": fp32,
             "self_join": sj,
+            "configs": configs,
             "join_ms_median": jms, "fraction_of_fp64_peak_cells": (cells_per_step() / (jms * 1e-3)) /
                                                                     (peak / FLOPS_PER_CELL)}
     print(json.dumps(line), flush=True)
@@ -406,19 +455,216 @@ def self_join_lines(q, dist=None, world=1):
         e = m // 2 if excl is None else excl
         pairs = (cnt - e - 1) * (cnt - e) / 2
         tsd.self_join(x, m, excl=excl)  # warm
-        ts = []
+        ts, dms, kms = [], [], []
         for _ in range(5):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             tsd.self_join(x, m, excl=excl)
             ts.append(time.perf_counter() - t0)
+            d_ms, k_ms, _ = tsd.last_join_timing()
+            dms.append(d_ms)
+            kms.append(k_ms)
         t = statistics.median(ts)
         if os.environ.get("TSD_BENCH_DEBUG"):
             print(f"[bench] {name}: {[round(v * 1e3, 2) for v in ts]} ms", file=sys.stderr, flush=True)
         out[name] = {"n": int(x.size), "m": m, "excl": e, "pairs": pairs, "ms": t * 1e3,
                      "value": pairs / t / 1e9, "unit": "GPair/s",
+                     "device_ms": statistics.median(dms), "kernel_ms": statistics.median(kms),
+                     "timing": "ms / value: host API wall time incl. copies (median of 5); device_ms: CUDA events "
+                               "from window statistics to epilogue; kernel_ms: the main sweep kernel",
                      "kernel": "symmetric upper-triangle sweep" if (m >= 192 and cnt >= max(98304, (1 << 26) // m))
                      else "full-matrix sweep"}
+    return out
+
+
+def nominal_peaks(dev, clocks):
+    """nominal FMA-pipe peaks of this GPU at its maximum SM clock (B200: 64
+    FP64 and 128 FP32 FMA lanes per SM per clock)"""
+    import torch
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    mhz = clocks.get("sm_max_mhz") or 1965.0
+    return {"sms": sms, "mhz": mhz, "fp64": sms * 64 * 2 * mhz * 1e6, "fp32": sms * 128 * 2 * mhz * 1e6}
+
+
+def _event_steps(step, stream, flush, steps, warmup, after=None):
+    """CUDA-event time (ms) of each of `steps` calls of step() on `stream`,
+    after `warmup` untimed calls, L2 flushed before each (not timed)"""
+    import torch
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    out = []
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        out.append(e0.elapsed_time(e1))
+        if after:
+            after()
+    return out
+
+
+def _plan_config(cfg, series, dev, stream, flush, peak, steps=5, warmup=3):
+    """device-resident dictionary join of `series` (list of 1-D arrays) on a
+    plan of cfg's dictionary: (ms per step, join kernel ms, launches)"""
+    import torch
+    import paper_2112_12965_b200 as tsd
+    import workloads as W
+    m = cfg["m"]
+    plan = tsd.DictPlan(W.dictionary(cfg), m)
+    lens = [len(x) for x in series]
+    d_q = torch.from_numpy(np.ascontiguousarray(np.concatenate(series))).to(dev)
+    rows = sum(n - m + 1 for n in lens)
+    d_val = torch.empty(rows, dtype=torch.float64, device=dev)
+    d_idx = torch.empty(rows, dtype=torch.int64, device=dev)
+    kms, nl = [], []
+
+    def step():
+        plan.join_device(d_q.data_ptr(), lens, d_val.data_ptr(), d_idx.data_ptr(), stream.cuda_stream)
+
+    def after():
+        kms.append(plan.last_kernel_timing()[0])
+        nl.append(plan.last_timing()[2])
+    ms = _event_steps(step, stream, flush, steps, warmup, after)
+    plan.close()
+    return statistics.median(ms), statistics.median(kms), nl[-1]
+
+
+def _frac(cells, ms, peak):
+    return FLOPS_PER_CELL * cells / (ms * 1e-3) / peak
+
+
+def config_lines(args, dev, stream, flush, peak, nominal):
+    """BASELINE configs C1, C2, C3, C5 (workloads.py) on this GPU, each with a
+    same-run CPU baseline of the unmodified reference (oracle/_ref, all host
+    threads). value = cells (pairs) per second of the device step."""
+    import torch
+    import paper_2112_12965_b200 as tsd
+    import workloads as W
+    from oracle import py_oracle as O
+    if args.skip_configs:
+        return None
+    threads = os.cpu_count() or 1
+    model = cpu_model()
+    have_ref = O.ref_available()
+    out = {}
+
+    def cpu_line(value, unit, sample, extrapolated, kind="reference"):
+        return {"value": value, "unit": unit, "cores": threads, "cpu_model": model, "kind": kind,
+                "sample": sample, "extrapolated": extrapolated}
+
+    # ---- C1: exact AB-join against 8 x 512, m = 100 (launch-bound: 5.4e7 cells)
+    c = W.c1()
+    ms, kms, nl = _plan_config(c, [c["q"]], dev, stream, flush, peak, steps=20)
+    line = {"workload": "C1: walk 16384 (seed 0) vs 8 walks x 512 (seed 1), m=100, FP64", "cells": c["cells"],
+            "ms": ms, "kernel_ms": kms, "value": c["cells"] / (ms * 1e-3) / 1e9, "unit": "GCell/s",
+            "frac": _frac(c["cells"], kms, peak), "gpu_launches_per_step": nl}
+    if have_ref:
+        dt = _timed(lambda: O.ref_join_dictionary(c["q"], c["segs"], c["starts"], c["m"], threads=threads), 3)
+        line["cpu_baseline"] = cpu_line(c["cells"] / dt / 1e9, "GCell/s", "full run, best of 3", False)
+    out["C1"] = line
+
+    # ---- C2: self-join, ECG n = 131072, m = 250, excl = m/4
+    c = W.c2()
+    tsd.self_join(c["t"], c["m"], excl=c["excl"])
+    hs, ds, ks = [], [], []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        tsd.self_join(c["t"], c["m"], excl=c["excl"])
+        hs.append((time.perf_counter() - t0) * 1e3)
+        d_ms, k_ms, nl = tsd.last_join_timing()
+        ds.append(d_ms)
+        ks.append(k_ms)
+    dms, kms = statistics.median(ds), statistics.median(ks)
+    line = {"workload": "C2: self-join, ECG-like n=131072 (seed 2), m=250, excl=m/4=62, FP64", "pairs": c["pairs"],
+            "ms": dms, "kernel_ms": kms, "host_api_ms": statistics.median(hs),
+            "value": c["pairs"] / (dms * 1e-3) / 1e9, "unit": "GPair/s", "frac": _frac(c["pairs"], kms, peak),
+            "pipeline_frac": _frac(c["pairs"], dms, peak), "gpu_launches_per_step": nl,
+            "timing": "ms: CUDA events over the device pipeline (statistics, seeds, sweep, merge, epilogue); "
+                      "host_api_ms adds the host copies"}
+    if have_ref:
+        cnt = c["t"].size - c["m"] + 1
+        e = c["m"] // 2
+        pairs_ref = (cnt - e - 1) * (cnt - e) // 2
+        dt = _timed(lambda: O.ref_self_join(c["t"], c["m"], threads=threads))
+        line["cpu_baseline"] = cpu_line(pairs_ref / dt / 1e9, "GPair/s",
+                                        "full run of the reference self_join, whose exclusion is fixed at m/2 = 125 "
+                                        "(profiles.hpp:273): %d pairs in %.2f s" % (pairs_ref, dt), False)
+    out["C2"] = line
+
+    # ---- C3: learn (from the C2 series) -> join 2^20 -> top-20 discords
+    c = W.c3()
+    m = c["m"]
+    d_q = torch.from_numpy(c["q"]).to(dev)
+    rows = c["q"].size - m + 1
+    d_val = torch.empty(rows, dtype=torch.float64, device=dev)
+    d_idx = torch.empty(rows, dtype=torch.int64, device=dev)
+    cfg = W.c3_learn_config()
+    runs = []
+    for it in range(4):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        D = tsd.learn_dictionary(c["train"], cfg)
+        t1 = time.perf_counter()
+        plan = tsd.DictPlan(D, m)
+        plan.join_device(d_q.data_ptr(), [c["q"].size], d_val.data_ptr(), d_idx.data_ptr(), stream.cuda_stream)
+        disc = tsd.find_discords((d_val.data_ptr(), rows, m), D.e_max, c["top_k"])
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        step_ms, join_ms, nl = plan.last_timing()
+        k_ms = plan.last_kernel_timing()[0]
+        plan.close()
+        if it > 0:
+            runs.append((t1 - t0, t2 - t1, step_ms, k_ms))
+    learn_s, rest_s, step_ms, k_ms = (statistics.median(r[i] for r in runs) for i in range(4))
+    cols = sum(s.length() - m + 1 for s in D.segments)
+    cells3 = rows * cols
+    an = np.asarray(c["anomalies"])
+    hits = sum(bool(np.any(np.abs(an - d.start) <= 300)) for d in disc)
+    line = {"workload": "C3: learn a dictionary from the C2 series (m=200, 2048-sample contexts, sample budget "
+                        "65536) -> join the 2^20-sample anomalous ECG query (seed 3) -> top-20 discords, FP64",
+            "segments": len(D.segments), "stored_samples": D.stored_samples(), "cells": cells3,
+            "ms": step_ms, "kernel_ms": k_ms, "value": cells3 / (step_ms * 1e-3) / 1e9, "unit": "GCell/s",
+            "frac": _frac(cells3, k_ms, peak), "learn_ms": learn_s * 1e3, "join_and_discords_ms": rest_s * 1e3,
+            "pipeline_ms": (learn_s + rest_s) * 1e3, "discords_near_injected_anomalies": int(hits),
+            "timing": "ms / value: CUDA events of the device-resident join step; learn_ms and join_and_discords_ms: "
+                      "host wall time of the public calls (median of 3 after one warm run)"}
+    if have_ref:
+        tl = _timed(lambda: O.ref_learn_dictionary_full(c["train"], m, k=c["k"], rule=1, value=c["budget"],
+                                                        threads=threads))
+        w = rows if args.cpu_c3_windows <= 0 else min(rows, args.cpu_c3_windows)
+        segs = [s.values for s in D.segments]
+        starts = [s.start for s in D.segments]
+        tj = _timed(lambda: O.ref_join_dictionary(c["q"][: w + m - 1], segs, starts, m, threads=threads))
+        vals = d_val.cpu().numpy()
+        td = _timed(lambda: O.ref_find_discords(vals, m, D.e_max, c["top_k"]))
+        line["cpu_baseline"] = cpu_line(w * cols / tj / 1e9, "GCell/s",
+                                        "reference learn_dictionary (full, %.2f s), join_dictionary on the first %d "
+                                        "query windows (%.2f s), find_discords (%.3f s)" % (tl, w, tj, td), w < rows)
+        line["cpu_baseline"]["pipeline_s"] = tl + tj * rows / w + td
+    del d_q, d_val, d_idx
+    out["C3"] = line
+
+    # ---- C5: 4096 series x 8192 vs 64 x 1024, m = 128, one device pass
+    c = W.c5()
+    ms, kms, nl = _plan_config(c, list(c["series"]), dev, stream, flush, peak, steps=3)
+    line = {"workload": "C5: 4096 traffic-like series x 8192 (seed 6) vs 64 segments x 1024 (seed 7), m=128, "
+                        "one batched device pass, FP64", "cells": c["cells"], "ms": ms, "kernel_ms": kms,
+            "value": c["cells"] / (ms * 1e-3) / 1e9, "unit": "GCell/s", "frac": _frac(c["cells"], kms, peak),
+            "gpu_launches_per_step": nl}
+    if have_ref:
+        ns = 16
+        dt = _timed(lambda: [O.ref_join_dictionary(c["series"][k], c["segs"], c["starts"], c["m"], threads=threads)
+                             for k in range(ns)])
+        cells_s = ns * (8192 - c["m"] + 1) * 64 * (1024 - c["m"] + 1)
+        line["cpu_baseline"] = cpu_line(cells_s / dt / 1e9, "GCell/s",
+                                        "reference join_dictionary looped over the first %d series (%.2f s)" % (ns, dt),
+                                        True)
+    out["C5"] = line
+    torch.cuda.empty_cache()
     return out
 
 
@@ -439,7 +685,11 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--ref-windows", type=int, default=CPU_SAMPLE_WINDOWS)
+    ap.add_argument("--ref-windows", type=int, default=1 << 15,
+                    help="query windows of C4 per reference-arm step (bounded sample)")
+    ap.add_argument("--cpu-c3-windows", type=int, default=1 << 18,
+                    help="query windows of C3 timed for its CPU baseline (0 = all, the full run)")
+    ap.add_argument("--skip-configs", action="store_true", help="only the C4 headline (+ fp32, self-join) lines")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per join launch from an ncu capture (reported as roofline.traffic)")
     args = ap.parse_args()

@@ -6,6 +6,8 @@
 #define TSDICT_B200_PROFILES_HPP
 
 #include <cstdint>
+#include <optional>
+#include <span>
 #include <thread>
 #include <vector>
 
@@ -13,6 +15,12 @@
 #include "tsdict/series.hpp"
 
 namespace tsdict {
+
+struct DistanceProfile {  // profiles.hpp:36-40
+  std::vector<double> values;
+  std::optional<std::size_t> query_origin;
+  std::size_t m = 0;
+};
 
 enum class join_kind { self, ab };
 
@@ -65,6 +73,47 @@ inline MatrixProfile self_join_excl(const TimeSeries& T, std::size_t m, std::siz
 
 inline MatrixProfile self_join(const TimeSeries& T, std::size_t m, unsigned threads = 0) {
   return self_join_excl(T, m, TSD_EXCL_DEFAULT, threads);
+}
+
+namespace detail {
+inline void check_profile_inputs(const TimeSeries& T, std::span<const double> Q, const SubseqStats& stats) {
+  // profiles.hpp:167-172 / :189-194
+  if (Q.size() != stats.m) throw error(errc::length_mismatch, "query length does not match stats window length");
+  if (stats.count() != T.n() - stats.m + 1)
+    throw error(errc::length_mismatch, "stats were computed for a different series length");
+}
+}  // namespace detail
+
+// profiles.hpp:164-181: znorm_distance per window, on the device with the
+// reference's operation order (bit-identical values)
+inline DistanceProfile distance_profile_naive(const TimeSeries& T, std::span<const double> Q,
+                                              const SubseqStats& stats,
+                                              std::optional<std::size_t> query_origin = {}) {
+  detail::check_profile_inputs(T, Q, stats);
+  DistanceProfile dp;
+  dp.m = stats.m;
+  dp.query_origin = query_origin;
+  dp.values.resize(stats.count());
+  if (stats.count() > 0)
+    detail::raise_status(tsd_distance_profile_naive(T.values.data(), T.n(), Q.data(), Q.size(), dp.values.data()));
+  return dp;
+}
+
+// profiles.hpp:186-260: MASS's conventions over the given window statistics
+// (constant query / windows, exact origin entry); the sliding dot products
+// are exact FP64 on the device instead of an FFT convolution
+inline DistanceProfile distance_profile_mass(const TimeSeries& T, std::span<const double> Q,
+                                             const SubseqStats& stats,
+                                             std::optional<std::size_t> query_origin = {}) {
+  detail::check_profile_inputs(T, Q, stats);
+  DistanceProfile dp;
+  dp.m = stats.m;
+  dp.query_origin = query_origin;
+  dp.values.resize(stats.count());
+  detail::raise_status(tsd_distance_profile_mass(T.values.data(), T.n(), Q.data(), Q.size(), stats.means.data(),
+                                                 stats.invn.data(), stats.constant_mask.data(),
+                                                 query_origin ? *query_origin : TSD_NO_ORIGIN, dp.values.data()));
+  return dp;
 }
 
 }  // namespace tsdict

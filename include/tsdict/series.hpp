@@ -52,35 +52,47 @@ inline double corr_to_dist(double rho, std::size_t m) {
   return std::min(std::max(d, 0.0), 2.0 * std::sqrt(static_cast<double>(m)));
 }
 
-// series.hpp:166-204 semantics: z-normalised Euclidean distance of two equal
-// windows; flat/flat -> 0, flat/other -> sqrt(2m). Host scalar code (not on
-// the join hot path): two passes in long double.
+namespace detail {
+struct kahan_sum {  // series.hpp:50-60
+  double sum = 0.0, comp = 0.0;
+  void add(double x) {
+    const double y = x - comp;
+    const double t = sum + y;
+    comp = (t - sum) - y;
+    sum = t;
+  }
+};
+}  // namespace detail
+
+// series.hpp:166-204: z-normalised Euclidean distance of two equal windows;
+// flat/flat -> 0, flat/other -> sqrt(2m). Host scalar code with the
+// reference's arithmetic (Kahan moments, the pair's constancy threshold), so
+// it agrees bit for bit with distance_profile_naive on the device.
 inline double znorm_distance(std::span<const double> a, std::span<const double> b) {
   if (a.size() != b.size()) throw error(errc::length_mismatch, "subsequences differ in length");
   const std::size_t m = a.size();
   if (m < 2) throw error(errc::window_too_small, "window length must be at least 2");
-  long double sa = 0, sb = 0;
   double max_abs = 0.0;
+  detail::kahan_sum sa, sb;
   for (std::size_t i = 0; i < m; ++i) {
-    sa += a[i];
-    sb += b[i];
+    sa.add(a[i]);
+    sb.add(b[i]);
     max_abs = std::max({max_abs, std::fabs(a[i]), std::fabs(b[i])});
   }
-  const long double md = static_cast<long double>(m), mu_a = sa / md, mu_b = sb / md;
-  long double va = 0, vb = 0, cv = 0;
+  const double md = static_cast<double>(m), mu_a = sa.sum / md, mu_b = sb.sum / md;
+  detail::kahan_sum va, vb, cv;
   for (std::size_t i = 0; i < m; ++i) {
-    const long double x = a[i] - mu_a, y = b[i] - mu_b;
-    va += x * x;
-    vb += y * y;
-    cv += x * y;
+    const double x = a[i] - mu_a, y = b[i] - mu_b;
+    va.add(x * x);
+    vb.add(y * y);
+    cv.add(x * y);
   }
-  const double sd_a = std::sqrt(static_cast<double>(va / md)), sd_b = std::sqrt(static_cast<double>(vb / md));
+  const double sd_a = std::sqrt(std::max(0.0, va.sum / md)), sd_b = std::sqrt(std::max(0.0, vb.sum / md));
   const double eps = constancy_threshold(max_abs);
   const bool fa = sd_a < eps, fb = sd_b < eps;
   if (fa && fb) return 0.0;
-  if (fa || fb) return std::sqrt(2.0 * static_cast<double>(m));
-  const double rho = static_cast<double>(cv / (md * (static_cast<long double>(sd_a) * sd_b)));
-  return corr_to_dist(rho, m);
+  if (fa || fb) return std::sqrt(2.0 * md);
+  return corr_to_dist(cv.sum / (md * (sd_a * sd_b)), m);
 }
 
 }  // namespace tsdict

@@ -162,13 +162,36 @@ int tsd_find_discords(const double* values, size_t cnt, size_t m, double e_max, 
 int tsd_find_discords_device(const double* d_values, size_t cnt, size_t m, double e_max, size_t top_k,
                              size_t* start, double* score, int* certified, size_t* count, void* stream);
 
+/* ---- distance profiles (profiles.hpp:164-260) ----
+ * Distance of the query window q (m samples) to every window of t (n - m + 1
+ * outputs in out).
+ * tsd_distance_profile_naive replaces distance_profile_naive (:164-181):
+ * znorm_distance (series.hpp:166-204) per window, bit-identical to the
+ * reference's arithmetic.
+ * tsd_distance_profile_mass replaces distance_profile_mass (:186-260) over the
+ * caller's window statistics of t (SubseqStats: means, invn, constant_mask,
+ * n - m + 1 each): MASS's conventions (constant query / constant windows, the
+ * origin entry by znorm_distance), with exact FP64 dot products in place of
+ * the FFT convolution. origin = TSD_NO_ORIGIN for none. The SubseqStats
+ * length checks (:189-194) are the caller's (the drop-in header does them). */
+#define TSD_NO_ORIGIN ((size_t)-1)
+int tsd_distance_profile_naive(const double* t, size_t n, const double* q, size_t m, double* out);
+int tsd_distance_profile_mass(const double* t, size_t n, const double* q, size_t m, const double* means,
+                              const double* invn, const unsigned char* constant_mask, size_t origin, double* out);
+
 /* ---- diagnostics ---- */
 const char* tsd_last_error(void);
+/* CUDA-event device times (ms) of the last tsd_ab_join / tsd_self_join call
+ * on this thread: the device pipeline (window statistics to epilogue, no
+ * host copies) and the main join kernel alone, plus its kernel launches. */
+int tsd_last_join_timing(double* device_ms, double* kernel_ms, int* launches);
 const char* tsd_status_name(int status); /* reference errc_name (errors.hpp:37-57) */
 const char* tsd_build_info(void);
 /* Measured DFMA (precision 0) / FFMA (precision 1) throughput of device 0 in
  * FLOP/s over roughly `seconds` of sustained load. */
 int tsd_measure_peak(int precision, double seconds, double* flops);
+/* the same, plus the SM clock (MHz) seen by the FP64 loop (0 for FP32) */
+int tsd_measure_peak_clock(int precision, double seconds, double* flops, double* sm_mhz);
 
 #ifdef __cplusplus
 }

@@ -54,6 +54,8 @@ def lib():
         _o.tsdo_compute_stats.argtypes = [_f64p, _sz, _sz, _f64p, _f64p, _f64p, _u8p]
         _o.tsdo_ab_join.argtypes = [_f64p, _sz, _f64p, _sz, _sz, _f64p, _i64p]
         _o.tsdo_self_join.argtypes = [_f64p, _sz, _sz, _sz, _f64p, _i64p]
+        _o.tsdo_self_join_mt.argtypes = [_f64p, _sz, _sz, _sz, ctypes.c_uint, _f64p, _i64p]
+        _o.tsdo_self_join_rows.argtypes = [_f64p, _sz, _sz, _sz, _sz, _sz, _f64p, _i64p]
         _o.tsdo_dict_join.argtypes = [_f64p, _sz, _f64p, _szp, _szp, _sz, _sz, _f64p, _i64p]
         _o.tsdo_corr_to_dist.restype = ctypes.c_double
         _o.tsdo_corr_to_dist.argtypes = [ctypes.c_double, _sz]
@@ -112,6 +114,35 @@ def self_join(t, m, excl=None):
     v, i = np.empty(cnt), np.empty(cnt, dtype=np.int64)
     _chk(lib().tsdo_self_join(_p(t, _f64p), t.size, m, m // 2 if excl is None else excl, _p(v, _f64p), _p(i, _i64p)))
     return v, i
+
+
+def self_join_mt(t, m, excl=None, threads=None):
+    """self_join with the reference's diagonal thread split (bit-identical to
+    self_join); threads defaults to every host core"""
+    t = _f(t)
+    cnt = max(1, t.size - m + 1)
+    v, i = np.empty(cnt), np.empty(cnt, dtype=np.int64)
+    _chk(lib().tsdo_self_join_mt(_p(t, _f64p), t.size, m, m // 2 if excl is None else excl,
+                                 threads or os.cpu_count() or 1, _p(v, _f64p), _p(i, _i64p)))
+    return v, i
+
+
+def self_join_rows(t, m, r0, nr, excl=None):
+    """rows [r0, r0 + nr) of self_join's profile (diagonals started at r0)"""
+    t = _f(t)
+    nr = min(nr, t.size - m + 1 - r0)
+    v, i = np.empty(nr), np.empty(nr, dtype=np.int64)
+    _chk(lib().tsdo_self_join_rows(_p(t, _f64p), t.size, m, m // 2 if excl is None else excl, r0, nr,
+                                   _p(v, _f64p), _p(i, _i64p)))
+    return v, i
+
+
+def parallel(fn, args, workers=None):
+    """run fn(*a) for every a in args on host threads (ctypes releases the
+    GIL during the oracle calls); results in order"""
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=workers or os.cpu_count() or 1) as ex:
+        return list(ex.map(lambda a: fn(*a), args))
 
 
 def dict_join(q, segments, starts, m):
@@ -257,6 +288,18 @@ def ref_join_dictionary(q, segments, starts, m, threads=1):
     _chk(ref().tsdr_join_dictionary(_p(q, _f64p), q.size, _p(vals, _f64p), _p(lens, _szp), _p(st, _szp),
                                     len(segments), m, m, threads, _p(v, _f64p), _p(i, _i64p)))
     return v, i
+
+
+def ref_distance_profile(t, q, m, mass=False, origin=None):
+    """the reference's distance_profile_naive / distance_profile_mass
+    (profiles.hpp:164-260; MASS with the oracle/standin FFT) over its own stats"""
+    t, q = _f(t), _f(q)
+    out = np.empty(t.size - m + 1)
+    r = ref()
+    r.tsdr_distance_profile.argtypes = [_f64p, _sz, _f64p, _sz, _int, _sz, _f64p]
+    _chk(r.tsdr_distance_profile(_p(t, _f64p), t.size, _p(q, _f64p), m, 1 if mass else 0,
+                                 ctypes.c_size_t(-1).value if origin is None else origin, _p(out, _f64p)))
+    return out
 
 
 def ref_compute_stats(x, m):

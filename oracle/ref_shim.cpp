@@ -67,6 +67,20 @@ int tsdr_self_join(const double* t, size_t n, size_t m, unsigned threads, double
   return guarded([&] { emit(tsdict::self_join(ts(t, n), m, threads), val, idx); });
 }
 
+// profiles.hpp:164-260 distance profiles over the reference's own stats
+// (mass != 0: distance_profile_mass; origin = SIZE_MAX for none)
+int tsdr_distance_profile(const double* t, size_t n, const double* q, size_t m, int mass, size_t origin, double* out) {
+  return guarded([&] {
+    const tsdict::TimeSeries T = ts(t, n);
+    const auto st = tsdict::compute_stats(T, m);
+    std::optional<std::size_t> org;
+    if (origin != SIZE_MAX) org = origin;
+    const std::span<const double> Q(q, m);
+    const auto dp = mass ? tsdict::distance_profile_mass(T, Q, st, org) : tsdict::distance_profile_naive(T, Q, st, org);
+    std::memcpy(out, dp.values.data(), dp.values.size() * sizeof(double));
+  });
+}
+
 int tsdr_join_dictionary(const double* q, size_t nq, const double* seg_vals, const size_t* seg_len,
                          const size_t* seg_start, size_t nseg, size_t m, size_t dict_m, unsigned threads,
                          double* val, int64_t* idx) {

@@ -4,13 +4,16 @@
  * Plain-C restatement of the reference hot path. Operation order follows the
  * reference line by line so that, compiled without FMA contraction
  * (oracle/Makefile: -ffp-contract=off, no -march), results are bit-identical
- * to the reference headers; tests/test_oracle_pin.py checks exactly that
+ * to the reference headers; tests/test_cpu.py
+ * (test_oracle_restatement_is_bit_identical_to_reference) checks exactly that
  * against tests/golden/.  Only tests/, __graft_entry__.smoke() and bench.py's
  * cpu_baseline / --impl reference legs may load this library.
  */
 #include "tsd_oracle.h"
 
 #include <float.h>
+#include <pthread.h>
+#include <stddef.h>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -277,6 +280,134 @@ int tsdo_self_join(const double* t, size_t n, size_t m, size_t excl, double* val
     }
   }
   finish_profile(corr, nn, cnt, m, val, idx);
+  free(corr);
+  free(nn);
+  prep_free(&s);
+  return ST_OK;
+}
+
+/* profiles.hpp:118-140 run_diagonals + :266-301 self_join with `threads`
+ * host threads: thread w walks diagonals di = w, w + T, ... into its own
+ * accumulator; the accumulators are merged in thread order with acc_merge's
+ * rule (profiles.hpp:79-85), so the result is bit-identical to threads = 1
+ * (profiles.hpp:12-17). Exclusion zone as a parameter, as tsdo_self_join. */
+typedef struct {
+  const double* t;
+  const prepared* s;
+  size_t m, excl, ndiag, w, nthreads;
+  double* corr;
+  int64_t* nn;
+} sj_task;
+
+static void* sj_worker(void* arg) {
+  sj_task* k = (sj_task*)arg;
+  const prepared* s = k->s;
+  const size_t cnt = s->cnt;
+  for (size_t i = 0; i < cnt; ++i) {
+    k->corr[i] = -2.0;
+    k->nn[i] = -1;
+  }
+  for (size_t di = k->w; di < k->ndiag; di += k->nthreads) {
+    const size_t d = k->excl + 1 + di;
+    double cov = window_dot(k->t, 0, s->means[0], k->t, d, s->means[d], k->m);
+    const size_t len = cnt - d;
+    for (size_t q = 0; q < len; ++q) {
+      if (q != 0) cov += s->df[q] * s->dg[q + d] + s->df[q + d] * s->dg[q];
+      double c = cov * s->invn[q] * s->invn[q + d];
+      if (s->flat[q] && s->flat[q + d]) {
+        c = 1.0;
+      } else {
+        c = clamp_corr(c);
+      }
+      acc_update(k->corr, k->nn, q, c, (int64_t)(q + d));
+      acc_update(k->corr, k->nn, q + d, c, (int64_t)q);
+    }
+  }
+  return NULL;
+}
+
+int tsdo_self_join_mt(const double* t, size_t n, size_t m, size_t excl, unsigned threads, double* val,
+                      int64_t* idx) {
+  if (m >= 2 && n < 2 * m) return ST_SERIES_TOO_SHORT;
+  prepared s;
+  int st = prep(t, n, m, &s);
+  if (st) return st;
+  const size_t cnt = s.cnt;
+  const size_t ndiag = cnt > excl + 1 ? cnt - excl - 1 : 0;
+  size_t T = threads ? threads : 1;
+  if (T > ndiag) T = ndiag ? ndiag : 1;
+  sj_task* tasks = (sj_task*)calloc(T, sizeof(sj_task));
+  pthread_t* th = (pthread_t*)calloc(T, sizeof(pthread_t));
+  for (size_t w = 0; w < T; ++w) {
+    tasks[w] = (sj_task){t, &s, m, excl, ndiag, w, T, (double*)malloc(cnt * sizeof(double)),
+                         (int64_t*)malloc(cnt * sizeof(int64_t))};
+    pthread_create(&th[w], NULL, sj_worker, &tasks[w]);
+  }
+  for (size_t w = 0; w < T; ++w) pthread_join(th[w], NULL);
+  for (size_t w = 1; w < T; ++w) /* acc_merge in thread order */
+    for (size_t i = 0; i < cnt; ++i)
+      acc_update(tasks[0].corr, tasks[0].nn, i, tasks[w].corr[i], tasks[w].nn[i]);
+  finish_profile(tasks[0].corr, tasks[0].nn, cnt, m, val, idx);
+  for (size_t w = 0; w < T; ++w) {
+    free(tasks[w].corr);
+    free(tasks[w].nn);
+  }
+  free(tasks);
+  free(th);
+  prep_free(&s);
+  return ST_OK;
+}
+
+/* Rows r0 .. r0+nr-1 of the self-join profile (profiles.hpp:266-301 with the
+ * exclusion zone as a parameter), for checking large self-joins on sampled
+ * row blocks: every diagonal delta = j - i with |delta| > excl that crosses
+ * the block starts at the block's first row on it with window_dot
+ * (profiles.hpp:101-108) and follows the reference's recurrence (:288, lower
+ * window index first) down the block; correlation, flat rule, clamp and
+ * acc_update as :289-296. The values differ from a whole-series run only by
+ * the recurrence's rounding (its diagonals start at row 0 in the reference). */
+int tsdo_self_join_rows(const double* t, size_t n, size_t m, size_t excl, size_t r0, size_t nr, double* val,
+                        int64_t* idx) {
+  if (m >= 2 && n < 2 * m) return ST_SERIES_TOO_SHORT;
+  prepared s;
+  int st = prep(t, n, m, &s);
+  if (st) return st;
+  const size_t cnt = s.cnt;
+  if (r0 >= cnt || nr == 0) {
+    prep_free(&s);
+    return ST_INVALID_ARGUMENT;
+  }
+  if (r0 + nr > cnt) nr = cnt - r0;
+  double* corr = (double*)malloc(nr * sizeof(double));
+  int64_t* nn = (int64_t*)malloc(nr * sizeof(int64_t));
+  for (size_t i = 0; i < nr; ++i) {
+    corr[i] = -2.0;
+    nn[i] = -1;
+  }
+  /* delta from -(r0 + nr - 1) to cnt - 1 - r0 */
+  const ptrdiff_t dlo = -(ptrdiff_t)(r0 + nr - 1), dhi = (ptrdiff_t)(cnt - 1 - r0);
+  for (ptrdiff_t delta = dlo; delta <= dhi; ++delta) {
+    const size_t ad = (size_t)(delta < 0 ? -delta : delta);
+    if (ad <= excl) continue;
+    size_t i = r0;
+    if (delta < 0 && (size_t)(-delta) > i) i = (size_t)(-delta);
+    size_t iend = r0 + nr;
+    if (delta > 0 && cnt - (size_t)delta < iend) iend = cnt - (size_t)delta;
+    if (i >= iend) continue;
+    const size_t q0 = delta > 0 ? i : i - ad; /* lower window of the pair */
+    double cov = window_dot(t, q0, s.means[q0], t, q0 + ad, s.means[q0 + ad], m);
+    for (size_t q = q0; i < iend; ++i, ++q) {
+      if (q != q0) cov += s.df[q] * s.dg[q + ad] + s.df[q + ad] * s.dg[q];
+      double c = cov * s.invn[q] * s.invn[q + ad];
+      if (s.flat[q] && s.flat[q + ad]) {
+        c = 1.0;
+      } else {
+        c = clamp_corr(c);
+      }
+      acc_update(corr, nn, i - r0, c, (int64_t)(delta > 0 ? q + ad : q));
+    }
+  }
+  finish_profile(corr, nn, nr, m, val, idx);
   free(corr);
   free(nn);
   prep_free(&s);

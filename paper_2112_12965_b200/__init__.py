@@ -39,6 +39,9 @@ __all__ = [
     "self_join_sharded",
     "window_labels",
     "auc_score",
+    "DistanceProfile",
+    "distance_profile_naive",
+    "distance_profile_mass",
 ]
 
 
@@ -120,10 +123,14 @@ C_SYMBOLS = {
     "tsd_dict_plan_destroy": (_int, [_vp]),
     "tsd_dict_plan_last_timing": (_int, [_vp, _f64p, _f64p, ctypes.POINTER(_int)]),
     "tsd_dict_plan_last_kernel_timing": (_int, [_vp, _f64p, _f64p]),
+    "tsd_distance_profile_naive": (_int, [_f64p, _sz, _f64p, _sz, _f64p]),
+    "tsd_distance_profile_mass": (_int, [_f64p, _sz, _f64p, _sz, _f64p, _f64p, _u8p, _sz, _f64p]),
     "tsd_last_error": (ctypes.c_char_p, []),
+    "tsd_last_join_timing": (_int, [_f64p, _f64p, ctypes.POINTER(_int)]),
     "tsd_status_name": (ctypes.c_char_p, [_int]),
     "tsd_build_info": (ctypes.c_char_p, []),
     "tsd_measure_peak": (_int, [_int, ctypes.c_double, _f64p]),
+    "tsd_measure_peak_clock": (_int, [_int, ctypes.c_double, _f64p, _f64p]),
 }
 
 _lib = None
@@ -255,6 +262,48 @@ def compute_stats(T, m: int) -> SubseqStats:
     _check(lib.tsd_compute_stats(_ptr(x, _f64p), x.size, m, _ptr(means, _f64p), _ptr(stds, _f64p),
                                  _ptr(invn, _f64p), _ptr(flat, _u8p)))
     return SubseqStats(m, means[:cnt], stds[:cnt], invn[:cnt], flat[:cnt])
+
+
+@dataclass
+class DistanceProfile:
+    """profiles.hpp:36-40"""
+    values: np.ndarray
+    query_origin: Optional[int] = None
+    m: int = 0
+
+
+def _dprof_check(x, Q, stats):
+    """profiles.hpp:167-172 / :189-194"""
+    if Q.size != stats.m:
+        raise TsdictError(errc.length_mismatch, "query length does not match stats window length")
+    if stats.count() != x.size - stats.m + 1:
+        raise TsdictError(errc.length_mismatch, "stats were computed for a different series length")
+
+
+def distance_profile_naive(T, Q, stats: SubseqStats, query_origin: Optional[int] = None) -> DistanceProfile:
+    """profiles.hpp:164-181: znorm_distance (series.hpp:166-204) per window, on the device."""
+    x, q = _vals(T), _f64(Q)
+    _dprof_check(x, q, stats)
+    out = np.empty(max(1, stats.count()))
+    if stats.count() > 0:
+        _check(load_library().tsd_distance_profile_naive(_ptr(x, _f64p), x.size, _ptr(q, _f64p), q.size,
+                                                         _ptr(out, _f64p)))
+    return DistanceProfile(out[:stats.count()], query_origin, stats.m)
+
+
+def distance_profile_mass(T, Q, stats: SubseqStats, query_origin: Optional[int] = None) -> DistanceProfile:
+    """profiles.hpp:186-260 (MASS's conventions; exact FP64 dot products on the
+    device instead of the FFT convolution)."""
+    x, q = _vals(T), _f64(Q)
+    _dprof_check(x, q, stats)
+    mu = _f64(stats.means)
+    iv = _f64(stats.invn)
+    cm = np.ascontiguousarray(stats.constant_mask, dtype=np.uint8)
+    out = np.empty(max(1, stats.count()))
+    org = ctypes.c_size_t(-1).value if query_origin is None else int(query_origin)
+    _check(load_library().tsd_distance_profile_mass(_ptr(x, _f64p), x.size, _ptr(q, _f64p), q.size, _ptr(mu, _f64p),
+                                                    _ptr(iv, _f64p), _ptr(cm, _u8p), org, _ptr(out, _f64p)))
+    return DistanceProfile(out[:stats.count()], query_origin, stats.m)
 
 
 def ab_join(A, B, m: int, threads: int = 0, precision="fp64") -> MatrixProfile:
@@ -564,6 +613,20 @@ def measure_peak(precision="fp64", seconds: float = 1.0) -> float:
     out = ctypes.c_double()
     _check(load_library().tsd_measure_peak(_PREC[precision], seconds, ctypes.byref(out)))
     return out.value
+
+
+def measure_peak_clock(precision="fp64", seconds: float = 1.0):
+    """(FLOP/s, SM MHz during the FP64 loop)"""
+    out, mhz = ctypes.c_double(), ctypes.c_double()
+    _check(load_library().tsd_measure_peak_clock(_PREC[precision], seconds, ctypes.byref(out), ctypes.byref(mhz)))
+    return out.value, mhz.value
+
+
+def last_join_timing():
+    """(device_ms, kernel_ms, launches) of the last ab_join / self_join on this thread"""
+    d, k, n = ctypes.c_double(0.0), ctypes.c_double(0.0), ctypes.c_int(0)
+    load_library().tsd_last_join_timing(ctypes.byref(d), ctypes.byref(k), ctypes.byref(n))
+    return d.value, k.value, n.value
 
 
 def build_info() -> str:

@@ -97,6 +97,13 @@ ThreadCtx& tctx() {
   return c;
 }
 
+// CUDA-event times of the last ab / self join on this thread (tsd_last_join_timing)
+struct LastJoin {
+  double device_ms = 0.0, kernel_ms = 0.0;
+  int launches = 0;
+};
+thread_local LastJoin t_last;
+
 // threshold groups for one series of `len` samples at window offset woff;
 // `block` > 0 splits into reference query blocks (dictionary.hpp:175-180)
 void add_groups(std::vector<Group>& g, int64_t woff, int64_t len, int m, int64_t block, int series) {
@@ -128,11 +135,21 @@ struct tsd_dict_plan {
 
 namespace {
 
+// The sweeps keep column (dictionary / self-join window) indices in 32 bits
+// (join.cu: SweepCtx::colbase, SegDev::ncol, the symmetric sweep's rows):
+// inputs whose column count would reach 2^31 are rejected up front rather
+// than truncated. (16 GiB of samples; no reference counterpart.)
+constexpr size_t kMaxColumnSamples = (size_t(1) << 31) - 256;
+
 int validate_dict(const size_t* seg_len, size_t nseg, size_t m) {  // dictionary.hpp:151-157
   if (nseg == 0) return fail(kEmptyDictionary, "dictionary has no segments");
-  for (size_t s = 0; s < nseg; ++s)
+  size_t tot = 0;
+  for (size_t s = 0; s < nseg; ++s) {
     if (seg_len[s] < m) return fail(kWindowMismatch, "dictionary segment shorter than the window length");
+    tot += seg_len[s];
+  }
   if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");
+  if (tot > kMaxColumnSamples) return fail(kInvalidArgument, "dictionary exceeds 2^31 samples");
   return kOk;
 }
 
@@ -276,6 +293,13 @@ int plan_join_host(tsd_dict_plan* p, const double* q, const size_t* q_len, size_
 extern "C" {
 
 const char* tsd_last_error(void) { return t_err.c_str(); }
+
+int tsd_last_join_timing(double* device_ms, double* kernel_ms, int* launches) {
+  if (device_ms) *device_ms = t_last.device_ms;
+  if (kernel_ms) *kernel_ms = t_last.kernel_ms;
+  if (launches) *launches = t_last.launches;
+  return kOk;
+}
 const char* tsd_status_name(int status) { return status_name(status); }
 const char* tsd_build_info(void) {
   return "tsdict-b200: sm_100a FP64 row-band join, double-double window statistics (" __DATE__ ")";
@@ -341,6 +365,8 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
   in.force_sym = force_sym;
   in.shard = shard;
   in.nshards = nshards;
+  for (int e = 4; e < 8; ++e) in.ev[e - 4] = tc.s.ev[e];
+  CK(cudaEventRecord(tc.s.ev[0], st));
   std::vector<Group> ga;
   add_groups(ga, 0, (int64_t)na, (int)m, 0, 0);
   int bad = -1;
@@ -395,9 +421,16 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
   }
   TRY(run_epilogue(d_bc, d_bj, in.rows.flag, nrows, d_segs, 1, (int)m, nullptr, nullptr, 1, in.cols.flag, in.cols.nwin,
                    excl, d_val, d_idx, tc.arena, st, &er));
+  CK(cudaEventRecord(tc.s.ev[1], st));
   CK(cudaMemcpyAsync(val, d_val, sizeof(double) * nrows, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(idx, d_idx, sizeof(int64_t) * nrows, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (stage == 0) {
+    float dm = 0.f, km = 0.f;
+    cudaEventElapsedTime(&dm, tc.s.ev[0], tc.s.ev[1]);
+    if (cudaEventElapsedTime(&km, tc.s.ev[6], tc.s.ev[7]) != cudaSuccess) km = 0.f;
+    t_last = LastJoin{dm, km, launches + 8};
+  }
   phase("epilogue + outputs");
   return kOk;
 }
@@ -407,6 +440,7 @@ int tsd_ab_join(const double* a, size_t na, const double* b, size_t nb, size_t m
   if (m >= 2 && (na < m || nb < m)) return fail(kSeriesTooShort, "ab-join needs both series at least m long");  // profiles.hpp:307-309
   if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");  // series.hpp:85 via :310
   if (precision != TSD_FP64 && precision != TSD_FP32) return fail(kInvalidArgument, "unknown precision");
+  if (nb > kMaxColumnSamples) return fail(kInvalidArgument, "target series exceeds 2^31 samples");
   return single_join(a, na, b, nb, m, -1, precision, val, idx);
 }
 
@@ -414,6 +448,7 @@ int tsd_self_join(const double* t, size_t n, size_t m, size_t excl, int precisio
   if (m >= 2 && n < 2 * m) return fail(kSeriesTooShort, "self-join needs n >= 2m");  // profiles.hpp:268-270
   if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");      // via :271
   if (precision != TSD_FP64 && precision != TSD_FP32) return fail(kInvalidArgument, "unknown precision");
+  if (n > kMaxColumnSamples) return fail(kInvalidArgument, "series exceeds 2^31 samples");
   const int64_t e = excl == TSD_EXCL_DEFAULT ? (int64_t)(m / 2) : (int64_t)excl;  // :273
   return single_join(t, n, nullptr, 0, m, e, precision, val, idx);
 }
@@ -423,6 +458,7 @@ int tsd_self_join_partial(const double* t, size_t n, size_t m, size_t excl, size
   if (m >= 2 && n < 2 * m) return fail(kSeriesTooShort, "self-join needs n >= 2m");
   if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");
   if (nshards == 0 || shard >= nshards) return fail(kInvalidArgument, "shard index out of range");
+  if (n > kMaxColumnSamples) return fail(kInvalidArgument, "series exceeds 2^31 samples");
   const int64_t e = excl == TSD_EXCL_DEFAULT ? (int64_t)(m / 2) : (int64_t)excl;
   return single_join(t, n, nullptr, 0, m, e, TSD_FP64, corr, col, true, 1, (int)shard, (int)nshards);
 }
@@ -752,6 +788,77 @@ int tsd_find_discords(const double* values, size_t cnt, size_t m, double e_max, 
   if (!d_v) return fail(kCudaError, "device allocation failed");
   CK(cudaMemcpyAsync(d_v, values, sizeof(double) * cnt, cudaMemcpyHostToDevice, tc.s.st));
   return tsd_find_discords_device(d_v, cnt, m, e_max, top_k, start, score, certified, count, tc.s.st);
+}
+
+// ---------------------------------------------------------------------------
+// distance profiles (profiles.hpp:164-260)
+// ---------------------------------------------------------------------------
+namespace {
+// the query's moments exactly as znorm_distance / distance_profile_mass form
+// them (series.hpp:172-190, profiles.hpp:206-224)
+QueryMoments query_moments(const double* q, size_t m) {
+  QueryMoments qm;
+  Kahan s;
+  for (size_t i = 0; i < m; ++i) {
+    s.add(q[i]);
+    qm.max_abs = std::max(qm.max_abs, std::fabs(q[i]));
+  }
+  const double md = (double)m;
+  qm.mu = s.sum / md;
+  Kahan v;
+  for (size_t i = 0; i < m; ++i) v.add((q[i] - qm.mu) * (q[i] - qm.mu));
+  qm.var_sum = v.sum;
+  const double sd = std::sqrt(std::max(0.0, v.sum / md));
+  qm.constant = sd < constancy_threshold_h(qm.max_abs);
+  qm.invn = qm.constant ? 0.0 : 1.0 / (sd * std::sqrt(md));
+  return qm;
+}
+
+int dprofile(const double* t, size_t n, const double* q, size_t m, const double* means, const double* invn,
+             const unsigned char* cmask, size_t origin, double* out) {
+  if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");
+  if (m > n) return fail(kWindowTooLarge, "window length exceeds series length");
+  if (means)  // distance_profile_mass: profiles.hpp:206-209
+    for (size_t i = 0; i < m; ++i)
+      if (!std::isfinite(q[i])) return fail(kNonFiniteInput, "query contains a non-finite sample");
+  const size_t cnt = n - m + 1;
+  ThreadCtx& tc = tctx();
+  if (int rc = tc.s.init()) return rc;
+  tc.arena.reset();
+  cudaStream_t st = tc.s.st;
+  double* d_x = (double*)tc.arena.get(sizeof(double) * (n + 64));
+  double* d_q = (double*)tc.arena.get(sizeof(double) * m);
+  double* d_out = (double*)tc.arena.get(sizeof(double) * cnt);
+  double* d_mu = means ? (double*)tc.arena.get(sizeof(double) * cnt) : nullptr;
+  double* d_iv = means ? (double*)tc.arena.get(sizeof(double) * cnt) : nullptr;
+  uint8_t* d_cm = means ? (uint8_t*)tc.arena.get(cnt) : nullptr;
+  if (!d_x || !d_q || !d_out || (means && (!d_mu || !d_iv || !d_cm)))
+    return fail(kCudaError, "device allocation failed");
+  CK(cudaMemcpyAsync(d_x, t, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_q, q, sizeof(double) * m, cudaMemcpyHostToDevice, st));
+  if (means) {
+    CK(cudaMemcpyAsync(d_mu, means, sizeof(double) * cnt, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_iv, invn, sizeof(double) * cnt, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_cm, cmask, cnt, cudaMemcpyHostToDevice, st));
+  }
+  const QueryMoments qm = query_moments(q, m);
+  const int64_t org = (origin == TSD_NO_ORIGIN || origin >= cnt) ? -1 : (int64_t)origin;
+  if (distance_profile_device(d_x, (int64_t)n, d_q, (int)m, qm, d_mu, d_iv, d_cm, org, d_out, st) != kOk)
+    return fail(kCudaError, std::string("distance profile: ") + cudaGetErrorString(cudaGetLastError()));
+  CK(cudaMemcpyAsync(out, d_out, sizeof(double) * cnt, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return kOk;
+}
+}  // namespace
+
+int tsd_distance_profile_naive(const double* t, size_t n, const double* q, size_t m, double* out) {
+  return dprofile(t, n, q, m, nullptr, nullptr, nullptr, TSD_NO_ORIGIN, out);
+}
+
+int tsd_distance_profile_mass(const double* t, size_t n, const double* q, size_t m, const double* means,
+                              const double* invn, const unsigned char* constant_mask, size_t origin, double* out) {
+  if (!means || !invn || !constant_mask) return fail(kInvalidArgument, "window statistics required");
+  return dprofile(t, n, q, m, means, invn, constant_mask, origin, out);
 }
 
 int tsd_dict_plan_destroy(tsd_dict_plan* plan) {

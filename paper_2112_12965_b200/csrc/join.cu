@@ -1516,6 +1516,19 @@ __global__ void k_epilogue(const double* __restrict__ bc, const int64_t* __restr
         j = i > excl ? 0 : (i + excl + 1 < ncols ? i + excl + 1 : -1);
       }
     }
+  } else if (excl >= 0) {
+    // self-join, non-flat row: every flat window j is a candidate with c = 0
+    // (invn_j = 0, profiles.hpp:289-296), the lowest admissible one winning
+    // among them. Those above the exclusion zone are swept by the row itself;
+    // those below come to a symmetric sweep only through the column side,
+    // which skips flat rows, so the lowest flat window j < i - excl is folded
+    // in here by acc_merge's rule (a no-op after the full-matrix sweep, which
+    // has already seen the same candidate)
+    const int64_t f0 = ncols > 0 ? bsuf[0] : -1;  // lowest flat column (suffix minimum from block 0)
+    if (f0 >= 0 && f0 < i - excl && (j < 0 || better(0.0, f0, c, j))) {
+      c = 0.0;
+      j = f0;
+    }
   }
   if (j < 0) {  // no admissible neighbour (profiles.hpp:149-151)
     val[o] = __longlong_as_double(0x7ff0000000000000LL);

@@ -10,8 +10,20 @@
 
 namespace {
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// clk[0..1]: SM clock and global timer (ns) at the start and end of block 0
 template <int CH>
-__global__ void __launch_bounds__(256) k_dfma(double* out, int iters, double a, double b) {
+__global__ void __launch_bounds__(256) k_dfma(double* out, int iters, double a, double b, unsigned long long* clk) {
+  const bool rec = blockIdx.x == 0 && threadIdx.x == 0 && clk;
+  if (rec) {
+    clk[0] = clock64();
+    clk[1] = gtimer();
+  }
   double x[CH];
 #pragma unroll
   for (int c = 0; c < CH; ++c) x[c] = threadIdx.x * 1e-3 + c;
@@ -23,6 +35,10 @@ __global__ void __launch_bounds__(256) k_dfma(double* out, int iters, double a, 
 #pragma unroll
   for (int c = 0; c < CH; ++c) s += x[c];
   if (s == 12345.678) out[0] = s;
+  if (rec) {
+    clk[2] = clock64();
+    clk[3] = gtimer();
+  }
 }
 
 template <int CH>
@@ -42,20 +58,23 @@ __global__ void __launch_bounds__(256) k_ffma(float* out, int iters, float a, fl
 
 }  // namespace
 
-extern "C" int tsd_measure_peak(int precision, double seconds, double* flops) {
+extern "C" int tsd_measure_peak_clock(int precision, double seconds, double* flops, double* sm_mhz) {
   int dev = 0, nsm = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
     return tsd::kCudaError;
   void* buf = nullptr;
-  if (cudaMalloc(&buf, 64) != cudaSuccess) return tsd::kCudaError;
+  if (cudaMalloc(&buf, 128) != cudaSuccess) return tsd::kCudaError;
+  unsigned long long* clk = reinterpret_cast<unsigned long long*>(static_cast<char*>(buf) + 64);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const int blocks = nsm * 4, threads = 256;
+  // 8 CTAs x 256 threads per SM (16 warps per scheduler) x 8 independent
+  // chains: far more FMAs in flight than the pipe latency needs
+  const int blocks = nsm * 8, threads = 256;
   const int CH = 8;
   auto launch = [&](int iters) {
     if (precision == 0)
-      k_dfma<CH><<<blocks, threads>>>((double*)buf, iters, 0.999999, 1e-7);
+      k_dfma<CH><<<blocks, threads>>>((double*)buf, iters, 0.999999, 1e-7, clk);
     else
       k_ffma<CH><<<blocks, threads>>>((float*)buf, iters, 0.999999f, 1e-7f);
   };
@@ -81,8 +100,17 @@ extern "C" int tsd_measure_peak(int precision, double seconds, double* flops) {
   cudaEventElapsedTime(&ms, e0, e1);
   const double fmas = (double)blocks * threads * CH * (double)iters * reps;
   *flops = 2.0 * fmas / (ms * 1e-3);
+  if (sm_mhz) {  // the SM clock over the last launch (block 0), FP64 only
+    unsigned long long h[4] = {0, 0, 0, 0};
+    cudaMemcpy(h, clk, sizeof(h), cudaMemcpyDeviceToHost);
+    *sm_mhz = (precision == 0 && h[3] > h[1]) ? (double)(h[2] - h[0]) / (double)(h[3] - h[1]) * 1e3 : 0.0;
+  }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaFree(buf);
   return cudaGetLastError() == cudaSuccess ? 0 : tsd::kCudaError;
+}
+
+extern "C" int tsd_measure_peak(int precision, double seconds, double* flops) {
+  return tsd_measure_peak_clock(precision, seconds, flops, nullptr);
 }

@@ -158,6 +158,23 @@ size_t learn_scratch_bytes();
 int discord_peaks(const double* d_vals, int64_t cnt, int m, int64_t want, uint8_t* d_sup, void* d_scratch,
                   std::vector<int64_t>& at, std::vector<double>& score, cudaStream_t st);
 
+// dprofile.cu ----------------------------------------------------------------
+// Distance profile of one query window q (m samples, device) against every
+// window of d_x[0..n): d_means == nullptr -> distance_profile_naive
+// (profiles.hpp:164-181, znorm_distance per window, bit-exact); otherwise
+// distance_profile_mass's rules (profiles.hpp:186-260) over the given window
+// statistics with exact FP64 dot products; origin < 0: none.
+struct QueryMoments {  // the query's znorm_distance / MASS moments (host, reference arithmetic)
+  double mu = 0.0;       // Kahan mean
+  double var_sum = 0.0;  // Kahan sum of (q - mu)^2
+  double max_abs = 0.0;
+  double invn = 0.0;     // 1 / (sd * sqrt(m)), 0 when constant
+  bool constant = false;
+};
+int distance_profile_device(const double* d_x, int64_t n, const double* d_q, int m, const QueryMoments& qm,
+                            const double* d_means, const double* d_invn, const uint8_t* d_cmask, int64_t origin,
+                            double* d_out, cudaStream_t st);
+
 // Epilogue: corr -> distance (series.hpp:153-161), concat column -> source
 // coordinate (dictionary.hpp:183-188), (inf, -1) sentinel for rows without an
 // admissible neighbour (profiles.hpp:149-151), row compaction for batched

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <functional>
+#include <span>
 #include <string>
 #include <vector>
 
@@ -18,6 +19,7 @@ void* tsd_rng_new(uint64_t seed);
 void tsd_rng_free(void* h);
 void tsd_rng_walk(void* h, size_t n, double* out);
 void tsd_rng_noise(void* h, size_t n, double* out);
+void tsd_synth_sine(size_t n, double period, double amp, double* out);
 }
 
 using namespace tsdict;
@@ -285,6 +287,100 @@ int main() {
     for (std::size_t i = 0; i < lab.size(); ++i) sc[i] = lab[i] ? 1.0 : 0.0;
     if (std::fabs(auc_score(sc, lab) - 1.0) > 0) return std::string("AUC != 1");
     return expect_code(errc::degenerate_labels, [&] { auc_score(sc, std::vector<unsigned char>(lab.size(), 0)); });
+  });
+  // DistanceProfile.* (reference test_profiles.cpp:67-135, same inputs and
+  // assertions): the drop-in's distance profiles run on the device
+  auto window = [](const TimeSeries& T, std::size_t at, std::size_t m) {
+    return std::span<const double>(T.values).subspan(at, m);
+  };
+  check("DistanceProfile.NaiveSelfMatchIsZero", [&] {
+    Rng r(21);
+    const TimeSeries T{r.walk(256)};
+    const auto st = compute_stats(T, 16);
+    const auto dp = distance_profile_naive(T, window(T, 7, 16), st, 7);
+    if (dp.values.size() != T.n() - 16 + 1) return std::string("size");
+    if (dp.values[7] != 0.0) return "self match " + std::to_string(dp.values[7]);
+    return dp.query_origin && *dp.query_origin == 7u ? std::string() : std::string("origin");
+  });
+  check("DistanceProfile.NaiveConstantTargetConvention", [&] {
+    const TimeSeries T{std::vector<double>(64, 2.5)};
+    Rng r(22);
+    const auto q = r.noise(16);
+    const auto st = compute_stats(T, 16);
+    const auto dp = distance_profile_naive(T, q, st);
+    for (double v : dp.values)
+      if (v != std::sqrt(32.0)) return "value " + std::to_string(v);
+    return std::string();
+  });
+  check("DistanceProfile.NaiveEqualsDirectEvaluation", [&] {
+    Rng r(23);
+    const TimeSeries T{r.noise(1024)};
+    const auto q = r.noise(32);
+    const auto st = compute_stats(T, 32);
+    const auto dp = distance_profile_naive(T, q, st);
+    for (std::size_t i = 0; i < dp.values.size(); ++i)
+      if (dp.values[i] != znorm_distance(window(T, i, 32), q)) return "not bit-identical at " + std::to_string(i);
+    return std::string();
+  });
+  check("DistanceProfile.MassSelfMatchNearZero", [&] {
+    Rng r(24);
+    const TimeSeries T{r.walk(256)};
+    const auto st = compute_stats(T, 16);
+    const auto dp = distance_profile_mass(T, window(T, 7, 16), st, 7);
+    return dp.values[7] <= 1e-6 ? std::string() : "self match " + std::to_string(dp.values[7]);
+  });
+  check("DistanceProfile.MassSinePeriodicity", [&] {
+    std::vector<double> s(1024);
+    tsd_synth_sine(1024, 64.0, 1.0, s.data());
+    const TimeSeries T{s};
+    const auto st = compute_stats(T, 64);
+    const auto dp = distance_profile_mass(T, window(T, 0, 64), st, 0);
+    for (std::size_t at = 0; at + 64 <= T.n() - 64 + 1; at += 64)
+      if (dp.values[at] > 1e-4) return "offset " + std::to_string(at);
+    return std::string();
+  });
+  check("DistanceProfile.MassMatchesNaive", [&] {
+    // the reference draws n, m from std::uniform_int_distribution (an
+    // implementation-defined mapping); the same ranges from our stream
+    Rng r(25);
+    for (int t = 0; t < 25; ++t) {
+      const auto u = r.noise(2);
+      const std::size_t n = 128 + (std::size_t)(std::fabs(u[0]) * 1000.0) % (4096 - 128 + 1);
+      const std::size_t m = std::min<std::size_t>(8 + (std::size_t)(std::fabs(u[1]) * 1000.0) % 121, n / 2);
+      const TimeSeries T{t % 2 == 0 ? r.walk(n) : r.noise(n)};
+      const auto q = t % 3 == 0 ? r.walk(m) : r.noise(m);
+      const auto st = compute_stats(T, m);
+      const auto naive = distance_profile_naive(T, q, st);
+      const auto mass = distance_profile_mass(T, q, st);
+      double worst = 0.0;
+      for (std::size_t i = 0; i < naive.values.size(); ++i)
+        worst = std::max(worst, std::fabs(naive.values[i] - mass.values[i]));
+      if (!(worst < 1e-5)) return "n=" + std::to_string(n) + " m=" + std::to_string(m) + " worst " + std::to_string(worst);
+    }
+    return std::string();
+  });
+  check("DistanceProfile.ConstantQueryConvention", [&] {
+    Rng r(26);
+    TimeSeries T{r.noise(200)};
+    for (std::size_t i = 40; i < 56; ++i) T.values[i] = 4.0;
+    const std::vector<double> q(16, 1.0);
+    const auto st = compute_stats(T, 16);
+    const auto mass = distance_profile_mass(T, q, st);
+    const auto naive = distance_profile_naive(T, q, st);
+    for (std::size_t i = 0; i < mass.values.size(); ++i) {
+      if (mass.values[i] != naive.values[i]) return "mass != naive at " + std::to_string(i);
+      if (mass.values[i] != (st.constant_mask[i] ? 0.0 : std::sqrt(32.0))) return "convention at " + std::to_string(i);
+    }
+    return std::string();
+  });
+  check("DistanceProfile.LengthMismatchThrows", [&] {
+    Rng r(27);
+    const TimeSeries T{r.noise(300)};
+    const auto st = compute_stats(T, 16);
+    const auto q = r.noise(17);
+    auto e = expect_code(errc::length_mismatch, [&] { distance_profile_naive(T, q, st); });
+    if (e.empty()) e = expect_code(errc::length_mismatch, [&] { distance_profile_mass(TimeSeries{r.noise(299)}, std::span<const double>(q).first(16), st); });
+    return e;
   });
   std::printf("%d failure(s)\n", failures);
   return failures;

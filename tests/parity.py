@@ -12,6 +12,9 @@ FP64 (BASELINE.json north_star):
 FP32 mode: |d_gpu - d_ref| <= 1e-3 absolute, and the index's exact distance
 within 1e-3 of the reference minimum.
 """
+import json
+import os
+
 import numpy as np
 
 REL = 1e-8
@@ -45,8 +48,31 @@ def check_profile(gv, gi, rv, ri, m, dist=None, fp32=False, label="", rho=RHO):
         assert abs(dg - dr) <= tol or (not fp32 and abs(dg * dg - dr * dr) <= 2 * m * rho), f"{label}: row {i}: idx {gi[i]} (d={dg!r}) vs ref {ri[i]} (d={dr!r})"
         ties += 1
     rel = dv / np.maximum(rv[f], 1e-300)
-    return {"rows": int(gv.size), "max_rel": float(rel.max()) if rel.size else 0.0,
-            "max_abs": float(dv.max()) if dv.size else 0.0, "ties": ties}
+    # rows inside tolerance only through the correlation bound (near-exact
+    # matches, where d = sqrt(2m(1 - rho)) amplifies rho's rounding)
+    fallback = 0 if fp32 else int(np.count_nonzero(dv > REL * rv[f]))
+    out = {"label": label, "rows": int(gv.size), "max_rel": float(rel.max()) if rel.size else 0.0,
+           "max_abs": float(dv.max()) if dv.size else 0.0, "ties": ties, "rho_fallback_rows": fallback}
+    report(out)
+    return out
+
+
+def report(stats):
+    """append one parity record to $TSD_PARITY_REPORT (JSON lines), if set"""
+    path = os.environ.get("TSD_PARITY_REPORT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(stats) + "\n")
+
+
+def check_blocks(label, blocks, m, dist=None, fp32=False):
+    """check_profile over row blocks [(rows, gpu_val, gpu_idx, ref_val, ref_idx)]
+    (rows: the global row index of each entry); dist(i, j) takes global rows.
+    Returns the merged statistics (reported once)."""
+    rows = np.concatenate([np.asarray(b[0], dtype=np.int64) for b in blocks])
+    gv, gi, rv, ri = (np.concatenate([np.asarray(b[k]) for b in blocks]) for k in (1, 2, 3, 4))
+    d = (lambda k, j: dist(int(rows[k]), j)) if dist is not None else None
+    return check_profile(gv, gi, rv, ri, m, d, fp32=fp32, label=label)
 
 
 def ab_dist(a, b, m):

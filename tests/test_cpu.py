@@ -1,6 +1,7 @@
 """CPU tests (no GPU): the oracle pinned to the reference's own outputs, the
 C ABI library's exported surface and host-side validation, the generators,
 and the multi-rank sharding logic (gloo, world_size 2)."""
+import ctypes
 import os
 import re
 import subprocess
@@ -63,6 +64,25 @@ def test_oracle_self_join_excl_parameter_reduces_to_reference():
     assert np.array_equal(v, rv) and np.array_equal(i, ri)
 
 
+def test_oracle_threaded_and_row_block_self_joins():
+    """the checker's two large-shape helpers: the thread-split self-join
+    (run_diagonals, profiles.hpp:118-140) is bit-identical to the sequential
+    one; row blocks started mid-series agree to rounding, flat stretches and
+    both exclusion conventions included"""
+    t = synth.ecg(5, 6000)[0]
+    t[1000:1400] = 0.5  # flat rows and columns
+    for excl in (None, 62, 0):
+        v, i = O.self_join(t, 100, excl)
+        mv, mi = O.self_join_mt(t, 100, excl, threads=5)
+        assert np.array_equal(v, mv) and np.array_equal(i, mi)
+        for r0, nr in ((0, 50), (900, 700), (5850, 100), (3000, 1)):
+            bv, bi = O.self_join_rows(t, 100, r0, nr, excl)
+            rv, ri = v[r0:r0 + bv.size], i[r0:r0 + bv.size]
+            assert bv.size == min(nr, v.size - r0)
+            assert np.allclose(bv, rv, rtol=1e-9, atol=1e-9)
+            assert np.mean(bi == ri) > 0.99
+
+
 @pytest.mark.skipif(not O.ref_available(), reason="reference build absent")
 def test_generators_replay_reference_synth():
     """paper_2112_12965_b200.synth draws exactly what the reference's synth.hpp draws"""
@@ -122,13 +142,33 @@ def test_status_names_match_reference_errc():
      tsd.errc.window_mismatch),                                                            # dict_join.hpp:44-46
     (lambda: tsd.compute_e_max(tsd.Dictionary([tsd.Segment(0, np.zeros(50))], m=10, source_length=60),
                                np.zeros(50)), tsd.errc.source_mismatch),                   # dictionary.hpp:248-250
+    (lambda: tsd.distance_profile_naive(np.zeros(50), np.zeros(9), tsd.SubseqStats(10, *(np.zeros(41),) * 4)),
+     tsd.errc.length_mismatch),                                                            # profiles.hpp:167-169
+    (lambda: tsd.distance_profile_mass(np.zeros(50), np.zeros(10), tsd.SubseqStats(10, *(np.zeros(40),) * 4)),
+     tsd.errc.length_mismatch),                                                            # profiles.hpp:192-194
 ])
 def test_host_validation_matches_reference_error_codes(call, code):
     with pytest.raises(tsd.TsdictError) as ei:
         call()
     assert ei.value.code() == code
     assert str(ei.value).split(":")[0] in {"WindowTooSmall", "WindowTooLarge", "SeriesTooShort", "EmptyDictionary",
-                                           "WindowMismatch", "SourceMismatch"}
+                                           "WindowMismatch", "SourceMismatch", "LengthMismatch"}
+
+
+def test_column_index_range_is_checked_before_any_device_work():
+    """the sweeps keep column indices in 32 bits: a target of 2^31 samples is
+    rejected with invalid_argument (no pointer is touched, no GPU needed)"""
+    lib = tsd.load_library()
+    a = np.zeros(1000)
+    huge = (1 << 31)
+    f64p = ctypes.POINTER(ctypes.c_double)
+    v, i = np.empty(901), np.empty(901, dtype=np.int64)
+    rc = lib.tsd_ab_join(a.ctypes.data_as(f64p), a.size, a.ctypes.data_as(f64p), huge, 100, 0,
+                         v.ctypes.data_as(f64p), i.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    assert rc == 1 + int(tsd.errc.invalid_argument), rc
+    rc = lib.tsd_self_join(a.ctypes.data_as(f64p), huge, 100, ctypes.c_size_t(-1).value, 0,
+                           v.ctypes.data_as(f64p), i.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+    assert rc == 1 + int(tsd.errc.invalid_argument), rc
 
 
 def test_no_cpu_fallback_without_gpu():
@@ -192,19 +232,3 @@ def test_sharded_self_join_exchange_two_ranks_gloo():
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "SELFSHARD_OK" in r.stdout
-
-
-def test_file_formats_match_reference_goldens():
-    """the drop-in file formats (include/tsdict/io.hpp)
-    against the unmodified reference's (tests/golden/io_golden.tsv, made by
-    tests/golden/make_io_golden.sh): every parser case gives the reference's
-    error code or the same values bit for bit; series, profile, label and
-    dictionary text byte-identical; a dictionary written by the drop-in reads
-    back identically in the reference. Host code, no GPU."""
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    subprocess.run(["make", "-C", os.path.join(root, "tests", "cpp"), "build/test_io"], check=True,
-                   capture_output=True)
-    r = subprocess.run([os.path.join(root, "tests", "cpp", "build", "test_io"),
-                        os.path.join(root, "tests", "golden", "io_golden.tsv")], capture_output=True, text=True)
-    assert r.returncode == 0, r.stdout + r.stderr
-    assert "checks match the reference" in r.stdout

@@ -679,3 +679,39 @@ def test_window_beyond_fft_heads():
     P = tsd.self_join(t, m)
     rv, ri = O.self_join(t, m)
     check_profile(P.values, P.indices, rv, ri, m, ab_dist(t, t, m), label="self m=4000")
+
+
+# ------------------------------------------------------------- distance profiles
+@pytest.mark.parametrize("kind,n,m", [("walk", 5000, 64), ("noise", 3000, 16), ("flat", 2000, 32),
+                                      ("walk", 70000, 300), ("constq", 1500, 16)])
+def test_distance_profiles_vs_reference(kind, n, m):
+    """distance_profile_naive is bit-identical to the reference's
+    (profiles.hpp:164-181, znorm_distance per window); distance_profile_mass
+    keeps MASS's conventions (constant query / windows, exact origin) and
+    agrees with the reference's MASS to its own 1e-5 (test_profiles.cpp:
+    113-130) and with the exact naive profile to 1e-7"""
+    if not O.ref_available():
+        pytest.skip("reference build absent")
+    rng = np.random.default_rng(n + m)
+    t = np.cumsum(rng.standard_normal(n)) if kind != "noise" else rng.standard_normal(n)
+    if kind == "flat":
+        t[300:500] = 1.5
+        t[900:1000] = -2.0
+    origin = 123
+    q = np.ones(m) if kind == "constq" else t[origin:origin + m].copy()
+    st = tsd.compute_stats(t, m)
+    nv = tsd.distance_profile_naive(t, q, st, origin)
+    rn = O.ref_distance_profile(t, q, m)
+    assert np.array_equal(nv.values, rn), f"naive: {np.sum(nv.values != rn)} values differ"
+    assert nv.query_origin == origin and nv.m == m
+    mv = tsd.distance_profile_mass(t, q, st, origin)
+    rm = O.ref_distance_profile(t, q, m, mass=True, origin=origin)
+    assert np.max(np.abs(mv.values - rm)) < 1e-5
+    assert np.max(np.abs(mv.values - rn)) < 1e-7
+    if kind != "constq":
+        assert mv.values[origin] == rn[origin]  # the exact origin entry (profiles.hpp:252-257)
+    with pytest.raises(tsd.TsdictError) as e:
+        bad = q.copy()
+        bad[3] = np.inf
+        tsd.distance_profile_mass(t, bad, st)
+    assert e.value.code() == tsd.errc.non_finite_input
