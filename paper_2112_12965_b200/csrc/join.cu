@@ -61,6 +61,9 @@ constexpr int T = 64;     // head / top-edge staging chunk (samples)
 #ifndef TSD_JOIN_MINB32
 #define TSD_JOIN_MINB32 7  // 7 CTAs: more registers for the 16-row FP32 lanes (C4 FP32 kernel 402 -> 388 ms)
 #endif
+#ifndef TSD_PIPE
+#define TSD_PIPE 1  // the software-pipelined FP64 sweep (sweep_segment_p) for the AB / full-matrix joins
+#endif
 #ifndef TSD_JOIN_MINB_SYM
 #define TSD_JOIN_MINB_SYM 7  // the symmetric sweep's column side wants ~146 registers (7 CTAs: 2^21 self-join -2.6 %)
 #endif
@@ -784,6 +787,175 @@ __device__ void sweep_segment(WarpSmem<R>& sm, const SweepCtx& cx, int lane, con
 }
 
 // ===========================================================================
+// Software-pipelined FP64 sweep (AB join and full-matrix self-join; the
+// default, TSD_PIPE=1). The step of column k computes the slot values of
+// column k into one register set from the other set (column k - 1) and only
+// THEN tests column k - 1: the high-word test -> vote -> branch chain no
+// longer sits between two steps' DFMAs, so a warp keeps issuing its next
+// column's 16 DFMAs while the previous column's test resolves. Two sets (PA
+// holds even columns, PB odd ones) replace the register rotation of
+// sweep_block: slot r of column k reads slot r - 1 of column k - 1 of the
+// other set, slot 0 the shuffled slot 7 of the lane above (lane 0: the band
+// above, through the edge ring). Everything else -- threshold blocks, the
+// shared exact update, chunk turns, edges -- is sweep_block's.
+// ===========================================================================
+template <int R>
+struct PipeState {
+  double PA[R], PB[R];  // column values: even columns in PA, odd in PB
+  double bKp[R];        // kplus(bestK)
+  int thr[R];           // hi(bKp * nmin) of the current threshold block
+  double dfb, dgb, e, in, nmin;  // prefetched column data / incoming diagonals of the next column
+  bool dirty;
+};
+
+// the high-word test of the column held in V (column c = k0 + uc, ring
+// position of its column data pos), then the exact update on a pass
+template <int R, bool SELF>
+__device__ __forceinline__ void pipe_test(WarpSmem<R>& sm, const SweepCtx& cx, int lane, PipeState<R>& S,
+                                          const double (&V)[R], int c, int pos) {
+  if (vote_any8(V, 0, S.thr)) [[unlikely]] {
+#ifdef TSD_COUNT_EXACT
+    if (lane == 0) atomicAdd(&g_exact_count, 1ull);
+#endif
+    const double invb = (&sm.colbuf[0][0])[pos].z;
+    bool may = false;
+#pragma unroll
+    for (int r = 0; r < R; ++r) may |= V[r] * invb > S.bKp[r] || !(S.bKp[r] > 0.0);
+    if (__any_sync(0xffffffffu, may)) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm.slide[r * 32 + lane] = V[r];
+      S.dirty |= exact_update64<R, SELF>(sm, lane, cx.colbase + c, invb, cx.row0, cx.excl);
+    }
+  }
+}
+
+// one block of R steps from column k0 (k0 % R == 0)
+template <int R, bool SELF, bool FIRST, bool GUARD>
+__device__ __forceinline__ void sweep_block_p(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int k0, int m96,
+                                              PipeState<R>& S, const double (&dfa)[R], const double (&dga)[R],
+                                              double* sbase, bool l0) {
+  static_assert(R == 8 && TB == R, "the pipelined sweep is written for R = 8 with one threshold block per 8 steps");
+  const int n = cx.ncol;
+  const double4* cflat = &sm.colbuf[0][0];
+  const double4* ccur = cflat + m96;
+  const double4* cnext = cflat + (m96 + R == 96 ? 0 : m96 + R);
+  double* const st_prev = sbase + (m96 == 0 ? 95 : m96 - 1);  // ring slot of column k0 - 1
+  double* const st_cur = sbase + m96;
+#pragma unroll
+  for (int u = 0; u < R; ++u) {
+    const int k = k0 + u;
+    if (GUARD && k >= n) break;
+    double(&D)[R] = (u & 1) ? S.PB : S.PA;  // column k
+    double(&V)[R] = (u & 1) ? S.PA : S.PB;  // column k - 1
+    if (FIRST && u == 0) {
+      // column 0 (the heads) is already in PA: its test runs at step 1
+      S.nmin = ccur[0].w;
+#pragma unroll
+      for (int r = 0; r < R; ++r) S.thr[r] = __double2hiint(S.bKp[r] * S.nmin);
+    } else {
+      // column k from column k - 1: slots 7..1 first (slot 7 feeds the next shuffle)
+#pragma unroll
+      for (int r = R - 1; r >= 1; --r) D[r] = __fma_rn(dga[r], S.dfb, __fma_rn(dfa[r], S.dgb, V[r - 1]));
+      const double x0 = l0 ? S.e : S.in;
+      D[0] = __fma_rn(dga[0], S.dfb, __fma_rn(dfa[0], S.dgb, x0));
+      // lane 31 retires its bottom row of column k - 1 into the edge ring
+      (u == 0 ? st_prev : st_cur + u - 1)[0] = V[R - 1];
+    }
+    // prefetch column k + 1: column data, lane 0's edge, the shuffled slot 7
+    if (!GUARD || k + 1 < n) {
+      const double4* cb = u + 1 < R ? ccur + u + 1 : cnext;
+      if ((u + 1) % TB == 0) {
+        const double4 c4 = *cb;
+        S.dfb = c4.x;
+        S.dgb = c4.y;
+        S.nmin = c4.w;  // consumed at the next block start, after this block's last test
+      } else {
+        const double2 c2 = *reinterpret_cast<const double2*>(cb);
+        S.dfb = c2.x;
+        S.dgb = c2.y;
+      }
+      S.e = sm.ering[m96 + u];
+    }
+    S.in = shfl_up1(D[R - 1]);
+    if (!(FIRST && u == 0)) {
+      // test column k - 1 with the thresholds of its block
+      pipe_test<R, SELF>(sm, cx, lane, S, V, k - 1, u == 0 ? (m96 == 0 ? 95 : m96 - 1) : m96 + u - 1);
+      if (u % TB == 0) {  // column k opens a threshold block: its thresholds, after the previous test
+        if (S.dirty) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) S.bKp[r] = kplus(sm.bK[r][lane]);
+          S.dirty = false;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) S.thr[r] = __double2hiint(S.bKp[r] * S.nmin);
+      }
+    }
+  }
+}
+template <int R, bool SELF>
+__device__ void sweep_segment_p(WarpSmem<R>& sm, const SweepCtx& cx, int lane, const double (&dfa)[R],
+                                const double (&dga)[R], PipeState<R>& S) {
+  const int n = cx.ncol;
+  const int nchunks = (n + 31) >> 5;
+  double* const sbase = lane == 31 ? sm.ering : sm.slide + 256;
+  const bool l0 = lane == 0;
+  __syncwarp();
+  issue_chunk(sm, cx, lane, 0);
+  if (nchunks > 1) issue_chunk(sm, cx, lane, 1); else cp_commit();
+  cp_wait<1>();
+  __syncwarp();
+  // column 1's data and lane 0's edge (step 0 of the first block prefetches them)
+  int flushed = 0;
+  auto chunk_turn = [&](int c) {
+    __syncwarp();
+    if (c >= 2 && cx.write_out) {
+      flush_block(sm, cx, lane, c - 2);
+      flushed = c - 1;
+    }
+    __syncwarp();
+    if (c + 1 < nchunks) issue_chunk(sm, cx, lane, c + 1); else cp_commit();
+    cp_wait<1>();
+    __syncwarp();
+  };
+  constexpr int BPC = 32 / R;
+  int k0 = 0, m96 = 0;
+  if (n <= R) {
+    sweep_block_p<R, SELF, true, true>(sm, cx, lane, 0, 0, S, dfa, dga, sbase, l0);
+  } else {
+    sweep_block_p<R, SELF, true, false>(sm, cx, lane, 0, 0, S, dfa, dga, sbase, l0);
+    int bic = 1;
+    k0 = R;
+    m96 = R;
+    for (; k0 + R <= n; k0 += R) {
+      if (bic == BPC - 1 && k0 + R < n) chunk_turn((k0 + R) >> 5);
+      sweep_block_p<R, SELF, false, false>(sm, cx, lane, k0, m96, S, dfa, dga, sbase, l0);
+      m96 = m96 + R == 96 ? 0 : m96 + R;
+      bic = bic == BPC - 1 ? 0 : bic + 1;
+    }
+    if (k0 < n) sweep_block_p<R, SELF, false, true>(sm, cx, lane, k0, m96, S, dfa, dga, sbase, l0);
+  }
+  // drain: the last column's test (its values sit in PA if its index is even)
+  {
+    const int c = n - 1;
+    const int pos = c % 96;  // ring position of column c
+    if (c & 1)
+      pipe_test<R, SELF>(sm, cx, lane, S, S.PB, c, pos);
+    else
+      pipe_test<R, SELF>(sm, cx, lane, S, S.PA, c, pos);
+  }
+  cp_wait<0>();
+  __syncwarp();
+#ifdef TSD_COUNT_EXACT
+  if (lane == 0) atomicAdd(&g_step_count, (unsigned long long)n);
+#endif
+  if (cx.write_out) {
+    const int last = (n - 2) >> 5;
+    for (int b = flushed; b <= last && n >= 2; ++b) flush_block(sm, cx, lane, b);
+  }
+  __syncwarp();
+}
+
+// ===========================================================================
 // FP32 mode: the same sweep with the column-normalised recurrence
 //   c~(i, k) = c~(i-1, k-1) * (s_k / s_{k-1}) + (df_a dg_b + dg_a df_b) * s_k,
 // s_k = invn_b[k], in packed fma.rn.f32x2 / mul.rn.f32x2 (FFMA2: two cells per
@@ -1274,6 +1446,21 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_
           }
           S.dirty = false;
           if constexpr (R == R32) sweep_segment32<SELF>(sm, cx, lane, FA, GA, S);
+        } else if (TSD_PIPE && !SYM) {
+          PipeState<R> S;
+          S.dirty = false;
+          double dfa[R], dga[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int64_t i = i0 + R * lane + r;
+            const bool in = i < a.nrows;
+            S.PA[r] = head[r];
+            S.PB[r] = 0.0;
+            dfa[r] = in ? a.dfa[i] : 0.0;
+            dga[r] = in ? a.dga[i] : 0.0;
+            S.bKp[r] = kplus(sm.bK[r][lane]);
+          }
+          if constexpr (R == 8) sweep_segment_p<R, SELF>(sm, cx, lane, dfa, dga, S);
         } else {
           SweepState<R> S;
           S.dirty = false;

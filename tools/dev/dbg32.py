@@ -1,5 +1,5 @@
 import sys, numpy as np
-import os; R = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, R)
+import os; R = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))); sys.path.insert(0, R)
 import paper_2112_12965_b200 as tsd
 from paper_2112_12965_b200 import synth
 from oracle import py_oracle as O

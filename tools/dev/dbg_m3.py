@@ -1,6 +1,6 @@
 """debug tiny-window AB-join mismatches (development tool)"""
 import sys, os
-R = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, R); sys.path.insert(0, R + "/tests")
+R = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))); sys.path.insert(0, R); sys.path.insert(0, R + "/tests")
 import numpy as np
 import paper_2112_12965_b200 as tsd
 from paper_2112_12965_b200 import synth

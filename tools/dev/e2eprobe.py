@@ -1,7 +1,7 @@
 """C4 end-to-end probe (development tool): tsd_dict_join with pinned host
 buffers, TSD_VERBOSE phases. usage: TSD_VERBOSE=1 python tools/e2eprobe.py [reps]"""
 import sys, os, time, ctypes
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import bench
 import paper_2112_12965_b200 as tsd

@@ -1,7 +1,7 @@
 """FP32 sweep A/B check (development tool): TSD_LIB_B vs the default library,
 bitwise, on several shapes. usage: TSD_LIB_B=... python tools/fp32cmp.py"""
 import sys, os, ctypes
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_2112_12965_b200 as t
 from paper_2112_12965_b200 import synth

@@ -1,7 +1,7 @@
 """C4 FP32-mode probe (development tool): device-resident plan joins, kernel
 timing, FP32 FFMA peak. usage: python tools/fp32probe.py [reps]"""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import bench
 import paper_2112_12965_b200 as tsd

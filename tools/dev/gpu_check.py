@@ -1,6 +1,6 @@
 """Quick GPU parity + timing probe (development tool)."""
 import sys, time, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_2112_12965_b200 as t
 from paper_2112_12965_b200 import synth

@@ -1,7 +1,7 @@
 """One dictionary join on device-resident inputs, for ncu (development tool).
 usage: python tools/profile_join.py NQ NSEG L M [reps]"""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import torch
 import paper_2112_12965_b200 as t

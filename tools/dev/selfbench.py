@@ -1,7 +1,7 @@
 """Self-join / long AB-join throughput probe (development tool).
 usage: python tools/selfbench.py [n ...]   (m = 256)"""
 import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_2112_12965_b200 as t
 from paper_2112_12965_b200 import synth

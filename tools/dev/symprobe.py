@@ -2,7 +2,7 @@
 query walk, m=512; BASELINE C2 ECG, m=250, excl=62), host API timing.
 usage: [TSD_LIB=...] [TSD_SYM=0|1] [TSD_VERBOSE=1] python tools/symprobe.py [reps]"""
 import sys, os, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np
 import paper_2112_12965_b200 as t
 from paper_2112_12965_b200 import synth

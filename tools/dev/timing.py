@@ -1,7 +1,7 @@
 """Timing probe: device-resident dictionary joins (development tool).
 usage: python tools/timing.py [configs...]  config = NQ:NSEG:L:M"""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
 import paper_2112_12965_b200 as t
 from paper_2112_12965_b200 import synth
