@@ -56,7 +56,7 @@ constexpr int TB = TSD_TB;  // threshold block (columns); nmin spans TB columns 
 constexpr int WARPS = TSD_WARPS;  // warps per CTA (independent; small CTAs give finer occupancy steps)
 constexpr int T = 64;     // head / top-edge staging chunk (samples)
 #ifndef TSD_JOIN_MINB
-#define TSD_JOIN_MINB 8  // 8 CTAs x 2 warps per SM: caps registers at 128
+#define TSD_JOIN_MINB 7  // 7 two-warp CTAs per SM (the pipelined sweep needs ~140 registers; 8 CTAs spill)
 #endif
 #ifndef TSD_JOIN_MINB32
 #define TSD_JOIN_MINB32 7  // 7 CTAs: more registers for the 16-row FP32 lanes (C4 FP32 kernel 402 -> 388 ms)

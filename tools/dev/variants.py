@@ -51,7 +51,7 @@ def main():
     res = {}
     base = None
     for lib in libs:
-        d = os.path.join(ROOT, "gpurun_out", "variants", os.path.basename(lib).replace(".so", ""))
+        d = os.path.join("/tmp", "tsd_variants", os.path.basename(lib).replace(".so", ""))
         os.makedirs(d, exist_ok=True)
         env = dict(os.environ, TSD_LIB=os.path.abspath(lib))
         r = subprocess.run([sys.executable, "-c", CHILD % (ROOT, cfgs, d)], env=env, capture_output=True, text=True)
