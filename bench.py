@@ -58,23 +58,6 @@ def workload_config():
             "l2": "query (128 MiB) + window stats exceed the 126 MB L2; L2 flushed with a 256 MiB write between steps"}
 
 
-# ---------------------------------------------------------------- sharding helpers (tests/_shard_worker.py)
-def shard_rows(nrows, rank, world):
-    """contiguous query-window range [lo, hi) of `rank`; its samples are
-    [lo, hi + m - 1) (m-1 halo), so shards need no exchange"""
-    per = (nrows + world - 1) // world
-    lo = min(nrows, rank * per)
-    return lo, min(nrows, lo + per)
-
-
-def gather_rows(val, idx, rank, world):
-    """gather per-rank profile slices to rank 0 (list of (val, idx) in rank order)"""
-    import torch.distributed as dist
-    obj = [None] * world
-    dist.all_gather_object(obj, (np.asarray(val), np.asarray(idx)))
-    return obj if rank == 0 else None
-
-
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region"""

@@ -77,6 +77,18 @@ int tsd_profile_merge(const double* corr_parts, const int64_t* col_parts, size_t
                       int64_t* col);
 int tsd_self_join_finish(const double* t, size_t n, size_t m, size_t excl, const double* corr, const int64_t* col,
                          double* val, int64_t* idx);
+/* The same three steps on DEVICE buffers (d_t: n samples; d_corr / d_col /
+ * d_val / d_idx: n-m+1 entries; parts: nparts x cnt, part p at [p * cnt]),
+ * queued on `stream` (a cudaStream_t) without host copies or synchronisation,
+ * so the exchange between them can be a device all-gather (NCCL). finish
+ * reads the merged partials from d_val / d_idx and overwrites them with the
+ * profile. */
+int tsd_self_join_partial_device(const double* d_t, size_t n, size_t m, size_t excl, size_t shard, size_t nshards,
+                                 double* d_corr, int64_t* d_col, void* stream);
+int tsd_profile_merge_device(const double* d_corr_parts, const int64_t* d_col_parts, size_t nparts, size_t cnt,
+                             double* d_corr, int64_t* d_col, void* stream);
+int tsd_self_join_finish_device(const double* d_t, size_t n, size_t m, size_t excl, double* d_val, int64_t* d_idx,
+                                void* stream);
 
 /* Replaces tsdict::detail::dict_min_profile (dictionary.hpp:149-193), the
  * engine of join_dictionary (dict_join.hpp:42-48) and compute_e_max
@@ -86,6 +98,14 @@ int tsd_self_join_finish(const double* t, size_t n, size_t m, size_t excl, const
  * segment boundaries are never formed. idx is in source coordinates. */
 int tsd_dict_join(const double* q, size_t nq, const double* seg_vals, const size_t* seg_len,
                   const size_t* seg_start, size_t nseg, size_t m, int precision, double* val, int64_t* idx);
+
+/* Row sharding of a dictionary join (multi-GPU): the query
+ * windows [*row_lo, *row_hi) of shard `shard` of `nshards`, whole
+ * 16384-window query blocks each (dictionary.hpp:175-180). Joining samples
+ * [row_lo, row_hi + m - 1) with tsd_dict_join gives exactly those rows of the
+ * unsharded profile's windows (indices are source coordinates); concatenating
+ * the shards in order is the whole profile. Host-only, no device work. */
+int tsd_dict_shard_rows(size_t nq, size_t m, size_t shard, size_t nshards, size_t* row_lo, size_t* row_hi);
 
 /* Batched form (no reference counterpart; equivalent to join_dictionary per
  * series): nseries query series packed back to back in q_vals (q_len[k]

@@ -37,6 +37,8 @@ __all__ = [
     "self_join_finish",
     "exchange_partials",
     "self_join_sharded",
+    "dict_shard_rows",
+    "join_dictionary_sharded",
     "window_labels",
     "auc_score",
     "DistanceProfile",
@@ -115,6 +117,10 @@ C_SYMBOLS = {
     "tsd_self_join_partial": (_int, [_f64p, _sz, _sz, _sz, _sz, _sz, _f64p, _i64p]),
     "tsd_profile_merge": (_int, [_f64p, _i64p, _sz, _sz, _f64p, _i64p]),
     "tsd_self_join_finish": (_int, [_f64p, _sz, _sz, _sz, _f64p, _i64p, _f64p, _i64p]),
+    "tsd_self_join_partial_device": (_int, [_vp, _sz, _sz, _sz, _sz, _sz, _vp, _vp, _vp]),
+    "tsd_profile_merge_device": (_int, [_vp, _vp, _sz, _sz, _vp, _vp, _vp]),
+    "tsd_self_join_finish_device": (_int, [_vp, _sz, _sz, _sz, _vp, _vp, _vp]),
+    "tsd_dict_shard_rows": (_int, [_sz, _sz, _sz, _sz, _szp, _szp]),
     "tsd_learn_dictionary": (_int, [_f64p, _sz, _sz, ctypes.c_double, _int, ctypes.c_double, _sz, _f64p, _szp, _szp,
                                     _f64p, _szp, _szp, _szp, _f64p, _f64p, ctypes.POINTER(_int)]),
     "tsd_dict_plan_create": (_int, [_f64p, _szp, _szp, _sz, _sz, _int, ctypes.POINTER(_vp)]),
@@ -486,11 +492,95 @@ def exchange_partials(corr, col, group=None):
 
 def self_join_sharded(T, m: int, excl: Optional[int] = None, group=None) -> MatrixProfile:
     """Self-join over the ranks of a torch.distributed group (one GPU each):
-    shard of the symmetric sweep, one all-gather, merge, finish."""
+    shard of the symmetric sweep, one all-gather, merge, finish.
+    NCCL groups keep everything on the device -- partials, the all-gather,
+    acc_merge (tsd_profile_merge_device) and the epilogue -- and copy only the
+    final profile to the host; other backends exchange host partials."""
+    import torch
     import torch.distributed as dist
-    corr, col = self_join_partial(T, m, excl, dist.get_rank(group), dist.get_world_size(group))
-    corr, col = exchange_partials(corr, col, group)
-    return self_join_finish(T, m, excl, corr, col)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if dist.get_backend(group) != "nccl":
+        corr, col = self_join_partial(T, m, excl, rank, world)
+        corr, col = exchange_partials(corr, col, group)
+        return self_join_finish(T, m, excl, corr, col)
+    x = _vals(T)
+    lib = load_library()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream(dev)
+    cnt = max(1, x.size - m + 1)
+    d_t = torch.from_numpy(x).to(dev)
+    pc = torch.empty(cnt, dtype=torch.float64, device=dev)
+    pj = torch.empty(cnt, dtype=torch.int64, device=dev)
+    e = _excl_arg(m, excl)
+    _check(lib.tsd_self_join_partial_device(d_t.data_ptr(), x.size, m, e, rank, world, pc.data_ptr(), pj.data_ptr(),
+                                            stream.cuda_stream))
+    allc = torch.empty(world * cnt, dtype=torch.float64, device=dev)
+    allj = torch.empty(world * cnt, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(allc, pc, group=group)
+    dist.all_gather_into_tensor(allj, pj, group=group)
+    _check(lib.tsd_profile_merge_device(allc.data_ptr(), allj.data_ptr(), world, cnt, pc.data_ptr(), pj.data_ptr(),
+                                        stream.cuda_stream))
+    _check(lib.tsd_self_join_finish_device(d_t.data_ptr(), x.size, m, e, pc.data_ptr(), pj.data_ptr(),
+                                           stream.cuda_stream))
+    stream.synchronize()
+    return MatrixProfile(values=pc.cpu().numpy(), indices=pj.cpu().numpy(), kind="self", m=m)
+
+
+def dict_shard_rows(nq: int, m: int, shard: int, nshards: int):
+    """[lo, hi) query windows of a row shard: whole 16384-window reference
+    blocks (dictionary.hpp:175-180), so the shard's statistics match the
+    unsharded join's (tsd_dict_shard_rows; host only)."""
+    lo, hi = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    _check(load_library().tsd_dict_shard_rows(nq, m, shard, nshards, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def join_dictionary_sharded(A, D: Dictionary, m: int, group=None, precision="fp64", _shard_join=None) -> MatrixProfile:
+    """join_dictionary with the query windows sharded over the ranks of a
+    torch.distributed group (one GPU each): each rank joins its
+    block-aligned row range on its device, one all-gather (NCCL, device
+    buffers) assembles the whole profile on every rank. Rows are independent:
+    no other exchange. (_shard_join(q_slice) -> (values, indices) replaces the
+    per-shard device join on non-NCCL groups; the gloo tests pass the oracle.)"""
+    import torch
+    import torch.distributed as dist
+    if m != D.m:
+        raise TsdictError(errc.window_mismatch, "requested window length differs from the dictionary's")
+    q = _vals(A)
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    cnt = q.size - m + 1
+    if m < 2 or cnt < 1:
+        return join_dictionary(A, D, m, precision=precision)  # the reference's errors
+    ranges = [dict_shard_rows(q.size, m, s, world) for s in range(world)]
+    per = max(1, max(hi - lo for lo, hi in ranges))
+    lo, hi = ranges[rank]
+    nccl = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device()) if nccl else torch.device("cpu")
+    v = torch.full((per,), float("inf"), dtype=torch.float64, device=dev)
+    j = torch.full((per,), -1, dtype=torch.int64, device=dev)
+    if hi > lo:
+        if nccl:
+            plan = DictPlan(D, m, precision)
+            d_q = torch.from_numpy(np.ascontiguousarray(q[lo:hi + m - 1])).to(dev)
+            plan.join_device(d_q.data_ptr(), [hi + m - 1 - lo], v.data_ptr(), j.data_ptr(),
+                             torch.cuda.current_stream(dev).cuda_stream)
+            plan.close()
+        else:
+            if _shard_join is not None:
+                pv, pi = _shard_join(q[lo:hi + m - 1])
+            else:
+                P = dict_min_profile(q[lo:hi + m - 1], D, m, precision=precision)
+                pv, pi = P.values, P.indices
+            v[: hi - lo] = torch.from_numpy(np.ascontiguousarray(pv, dtype=np.float64))
+            j[: hi - lo] = torch.from_numpy(np.ascontiguousarray(pi, dtype=np.int64))
+    av = torch.empty(world * per, dtype=torch.float64, device=dev)
+    aj = torch.empty(world * per, dtype=torch.int64, device=dev)
+    dist.all_gather_into_tensor(av, v, group=group)
+    dist.all_gather_into_tensor(aj, j, group=group)
+    av, aj = av.cpu().numpy(), aj.cpu().numpy()
+    vals = np.concatenate([av[s * per: s * per + (h - l)] for s, (l, h) in enumerate(ranges)])
+    idx = np.concatenate([aj[s * per: s * per + (h - l)] for s, (l, h) in enumerate(ranges)])
+    return MatrixProfile(vals, idx, "ab", m)
 
 
 @dataclass

@@ -338,13 +338,16 @@ int tsd_compute_stats(const double* x, size_t n, size_t m, double* means, double
 // stage 0: join + epilogue; 1: join only, val/idx receive the raw per-row
 // (corr, column) partials of shard `shard` of `nshards`; 2: epilogue only,
 // val/idx hold merged raw partials on input and the profile on output
+// device != nullptr: a, val and idx are DEVICE pointers (self-join only),
+// work is queued on *device (the caller's stream), nothing is copied through
+// the host and the call returns without synchronising
 static int single_join(const double* a, size_t na, const double* b, size_t nb, size_t m, int64_t excl, int precision,
                        double* val, int64_t* idx, bool force_sym = false, int stage = 0, int shard = 0,
-                       int nshards = 1) {
+                       int nshards = 1, const cudaStream_t* device = nullptr) {
   ThreadCtx& tc = tctx();
   if (int rc = tc.s.init()) return rc;
   tc.arena.reset();
-  cudaStream_t st = tc.s.st;
+  cudaStream_t st = device ? *device : tc.s.st;
   const bool self = (b == nullptr);
   const bool verbose = getenv("TSD_VERBOSE") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
@@ -354,11 +357,12 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
     fprintf(stderr, "[tsd] %s at %.2f ms\n", what,
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   };
-  double* d_a = (double*)tc.arena.get(sizeof(double) * (na + 64));
+  if (device && !self) return fail(kInvalidArgument, "device-resident joins are self-joins");
+  double* d_a = device ? const_cast<double*>(a) : (double*)tc.arena.get(sizeof(double) * (na + 64));
   double* d_b = self ? d_a : (double*)tc.arena.get(sizeof(double) * (nb + 64));
   if (self) nb = na;
   if (!d_a || !d_b) return fail(kCudaError, "device allocation failed");
-  CK(cudaMemcpyAsync(d_a, a, sizeof(double) * na, cudaMemcpyHostToDevice, st));
+  if (!device) CK(cudaMemcpyAsync(d_a, a, sizeof(double) * na, cudaMemcpyHostToDevice, st));
   if (!self) CK(cudaMemcpyAsync(d_b, b, sizeof(double) * nb, cudaMemcpyHostToDevice, st));
   Error er{0, ""};
   JoinInputs in;
@@ -390,17 +394,21 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
   in.excl = excl;
   in.precision = precision;
   const int64_t nrows = in.rows.nwin;
-  double* d_bc = (double*)tc.arena.get(sizeof(double) * nrows);
-  int64_t* d_bj = (int64_t*)tc.arena.get(sizeof(int64_t) * nrows);
-  double* d_val = (double*)tc.arena.get(sizeof(double) * nrows);
-  int64_t* d_idx = (int64_t*)tc.arena.get(sizeof(int64_t) * nrows);
+  // device mode: stage 1 writes the partials straight into val / idx, stage 2
+  // reads the merged partials from them and writes the profile in place
+  double* d_bc = device ? val : (double*)tc.arena.get(sizeof(double) * nrows);
+  int64_t* d_bj = device ? idx : (int64_t*)tc.arena.get(sizeof(int64_t) * nrows);
+  double* d_val = device ? val : (double*)tc.arena.get(sizeof(double) * nrows);
+  int64_t* d_idx = device ? idx : (int64_t*)tc.arena.get(sizeof(int64_t) * nrows);
   SegDev* d_segs = (SegDev*)tc.arena.get(sizeof(SegDev));
   if (!d_bc || !d_bj || !d_val || !d_idx || !d_segs) return fail(kCudaError, "device allocation failed");
   CK(cudaMemcpyAsync(d_segs, in.segs.data(), sizeof(SegDev), cudaMemcpyHostToDevice, st));
   int launches = 0;
   if (stage == 2) {
-    CK(cudaMemcpyAsync(d_bc, val, sizeof(double) * nrows, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_bj, idx, sizeof(int64_t) * nrows, cudaMemcpyHostToDevice, st));
+    if (!device) {
+      CK(cudaMemcpyAsync(d_bc, val, sizeof(double) * nrows, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(d_bj, idx, sizeof(int64_t) * nrows, cudaMemcpyHostToDevice, st));
+    }
   } else {
     TRY(run_join(in, d_bc, d_bj, tc.arena, st, &er, &launches));
     if (self && getenv("TSD_PERFECT_SEED")) {  // development probe: rerun seeded from the final bests
@@ -413,14 +421,25 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
     }
   }
   phase("join");
+  if (stage == 1 && device) return kOk;
   if (stage == 1) {
     CK(cudaMemcpyAsync(val, d_bc, sizeof(double) * nrows, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(idx, d_bj, sizeof(int64_t) * nrows, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return kOk;
   }
+  if (device && stage == 2) {  // the epilogue reads and writes the same rows: stage the partials
+    double* c2 = (double*)tc.arena.get(sizeof(double) * nrows);
+    int64_t* j2 = (int64_t*)tc.arena.get(sizeof(int64_t) * nrows);
+    if (!c2 || !j2) return fail(kCudaError, "device allocation failed");
+    CK(cudaMemcpyAsync(c2, d_bc, sizeof(double) * nrows, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(j2, d_bj, sizeof(int64_t) * nrows, cudaMemcpyDeviceToDevice, st));
+    d_bc = c2;
+    d_bj = j2;
+  }
   TRY(run_epilogue(d_bc, d_bj, in.rows.flag, nrows, d_segs, 1, (int)m, nullptr, nullptr, 1, in.cols.flag, in.cols.nwin,
                    excl, d_val, d_idx, tc.arena, st, &er));
+  if (device) return kOk;
   CK(cudaEventRecord(tc.s.ev[1], st));
   CK(cudaMemcpyAsync(val, d_val, sizeof(double) * nrows, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(idx, d_idx, sizeof(int64_t) * nrows, cudaMemcpyDeviceToHost, st));
@@ -491,6 +510,48 @@ int tsd_self_join_finish(const double* t, size_t n, size_t m, size_t excl, const
   std::copy(corr, corr + cnt, val);
   std::copy(col, col + cnt, idx);
   return single_join(t, n, nullptr, 0, m, e, TSD_FP64, val, idx, true, 2);
+}
+
+int tsd_self_join_partial_device(const double* d_t, size_t n, size_t m, size_t excl, size_t shard, size_t nshards,
+                                 double* d_corr, int64_t* d_col, void* stream) {
+  if (m >= 2 && n < 2 * m) return fail(kSeriesTooShort, "self-join needs n >= 2m");
+  if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");
+  if (nshards == 0 || shard >= nshards) return fail(kInvalidArgument, "shard index out of range");
+  if (n > kMaxColumnSamples) return fail(kInvalidArgument, "series exceeds 2^31 samples");
+  const int64_t e = excl == TSD_EXCL_DEFAULT ? (int64_t)(m / 2) : (int64_t)excl;
+  const cudaStream_t st = (cudaStream_t)stream;
+  return single_join(d_t, n, nullptr, 0, m, e, TSD_FP64, d_corr, d_col, true, 1, (int)shard, (int)nshards, &st);
+}
+
+int tsd_profile_merge_device(const double* d_corr_parts, const int64_t* d_col_parts, size_t nparts, size_t cnt,
+                             double* d_corr, int64_t* d_col, void* stream) {
+  if (nparts == 0) return fail(kInvalidArgument, "no partials");
+  if (profile_merge_device(d_corr_parts, d_col_parts, (int)nparts, (int64_t)cnt, d_corr, d_col,
+                           (cudaStream_t)stream) != kOk)
+    return fail(kCudaError, std::string("partial merge: ") + cudaGetErrorString(cudaGetLastError()));
+  return kOk;
+}
+
+int tsd_self_join_finish_device(const double* d_t, size_t n, size_t m, size_t excl, double* d_val, int64_t* d_idx,
+                                void* stream) {
+  if (m >= 2 && n < 2 * m) return fail(kSeriesTooShort, "self-join needs n >= 2m");
+  if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");
+  const int64_t e = excl == TSD_EXCL_DEFAULT ? (int64_t)(m / 2) : (int64_t)excl;
+  const cudaStream_t st = (cudaStream_t)stream;
+  return single_join(d_t, n, nullptr, 0, m, e, TSD_FP64, d_val, d_idx, true, 2, 0, 1, &st);
+}
+
+int tsd_dict_shard_rows(size_t nq, size_t m, size_t shard, size_t nshards, size_t* row_lo, size_t* row_hi) {
+  // whole 16384-window query blocks (dictionary.hpp:175-180) per shard, so a
+  // shard's window statistics group exactly as in the unsharded join
+  if (nshards == 0 || shard >= nshards) return fail(kInvalidArgument, "shard index out of range");
+  if (m < 2) return fail(kWindowTooSmall, "window length must be at least 2");
+  if (m > nq) return fail(kWindowTooLarge, "window length exceeds series length");
+  const size_t cnt = nq - m + 1, block = 16384, nb = (cnt + block - 1) / block;
+  const size_t b0 = nb * shard / nshards, b1 = nb * (shard + 1) / nshards;
+  *row_lo = std::min(cnt, b0 * block);
+  *row_hi = std::min(cnt, b1 * block);
+  return kOk;
 }
 
 int tsd_dict_join(const double* q, size_t nq, const double* seg_vals, const size_t* seg_len, const size_t* seg_start,

@@ -2536,6 +2536,34 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
   return launch_join<8, false, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
 }
 
+namespace {
+// acc_merge's rule over shard partials (profiles.hpp:79-85): larger corr,
+// then lower index; part p of row i at [p * cnt + i]
+__global__ void k_merge_parts(const double* __restrict__ pc, const int64_t* __restrict__ pj, int nparts, int64_t cnt,
+                              double* __restrict__ oc, int64_t* __restrict__ oj) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  double bc = -2.0;
+  int64_t bj = -1;
+  for (int p = 0; p < nparts; ++p) {
+    const double c = pc[(int64_t)p * cnt + i];
+    const int64_t j = pj[(int64_t)p * cnt + i];
+    if (j >= 0 && (bj < 0 || better(c, j, bc, bj))) {
+      bc = c;
+      bj = j;
+    }
+  }
+  oc[i] = bc;
+  oj[i] = bj;
+}
+}  // namespace
+
+int profile_merge_device(const double* d_pc, const int64_t* d_pj, int nparts, int64_t cnt, double* d_c, int64_t* d_j,
+                         cudaStream_t st) {
+  if (cnt > 0) k_merge_parts<<<(unsigned)((cnt + 255) / 256), 256, 0, st>>>(d_pc, d_pj, nparts, cnt, d_c, d_j);
+  return cudaGetLastError() == cudaSuccess ? kOk : kCudaError;
+}
+
 int run_epilogue(const double* d_best_c, const int64_t* d_best_j, const uint8_t* d_row_flag, int64_t nrows,
                  const SegDev* d_segs, int nseg, int m, const int64_t* d_woff, const int64_t* d_ooff, int nser,
                  const uint8_t* d_col_flag, int64_t ncols, int64_t excl, double* d_val, int64_t* d_idx, Arena& arena,

@@ -175,6 +175,10 @@ int distance_profile_device(const double* d_x, int64_t n, const double* d_q, int
                             const double* d_means, const double* d_invn, const uint8_t* d_cmask, int64_t origin,
                             double* d_out, cudaStream_t st);
 
+// acc_merge over nparts per-row partials [p * cnt + i] (sharded self-join)
+int profile_merge_device(const double* d_pc, const int64_t* d_pj, int nparts, int64_t cnt, double* d_c, int64_t* d_j,
+                         cudaStream_t st);
+
 // Epilogue: corr -> distance (series.hpp:153-161), concat column -> source
 // coordinate (dictionary.hpp:183-188), (inf, -1) sentinel for rows without an
 // admissible neighbour (profiles.hpp:149-151), row compaction for batched

@@ -183,12 +183,13 @@ def test_no_cpu_fallback_without_gpu():
 
 
 # ---------------------------------------------------------------- multi-rank logic
-def test_row_sharding_two_ranks_gloo():
-    """bench.py's row sharding (contiguous query ranges with m-1 halo, no
-    collective on the data path; results gathered to rank 0) reproduces the
-    single-rank profile. Per-shard compute uses the oracle (CPU test)."""
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29500 + os.getpid() % 1000))
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_shard_worker.py")], env=env,
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharding_gloo(world):
+    """join_dictionary_sharded over world_size 2 and 3 gloo groups: block-aligned
+    row shards (tsd_dict_shard_rows), one all-gather, bit-identical to the
+    unsharded join. Per-shard compute uses the oracle (CPU test)."""
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(29500 + world + os.getpid() % 1000))
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "_shard_worker.py"), str(world)], env=env,
                        capture_output=True, text=True, timeout=240)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "SHARD_OK" in r.stdout

@@ -7,6 +7,7 @@ oracle restatement at runtime for larger / BASELINE-shaped inputs; full-size
 configs are checked on sampled rows and through size-independent properties.
 Tolerances: tests/parity.py.
 """
+import ctypes
 import os
 import subprocess
 
@@ -631,6 +632,63 @@ def test_sharded_self_join_equals_unsharded(monkeypatch, nshards):
     corr, col = tsd.merge_partials([p[0] for p in parts], [p[1] for p in parts])
     P = tsd.self_join_finish(t, m, None, corr, col)
     assert np.array_equal(P.indices, ref.indices) and np.array_equal(P.values, ref.values)
+
+
+def test_sharded_self_join_device_path(monkeypatch):
+    """the device-resident sharded self-join (tsd_self_join_partial_device ->
+    device all-gather layout -> tsd_profile_merge_device ->
+    tsd_self_join_finish_device), shards run in turn on one GPU, equals the
+    unsharded symmetric self-join bitwise -- no host round trip between steps"""
+    import torch
+    monkeypatch.setenv("TSD_SYM", "1")
+    t = synth.walk(62, 50000)
+    t[20000:20400] = 1.0  # flat rows / columns through the device epilogue
+    m, S = 96, 3
+    ref = tsd.self_join(t, m)
+    lib = tsd.load_library()
+    cnt = t.size - m + 1
+    d_t = torch.from_numpy(t).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    parts_c = torch.empty(S * cnt, dtype=torch.float64, device="cuda")
+    parts_j = torch.empty(S * cnt, dtype=torch.int64, device="cuda")
+    for s in range(S):
+        rc = lib.tsd_self_join_partial_device(d_t.data_ptr(), t.size, m, ctypes.c_size_t(-1).value, s, S,
+                                              parts_c.data_ptr() + 8 * s * cnt, parts_j.data_ptr() + 8 * s * cnt, st)
+        assert rc == 0, lib.tsd_last_error()
+    c = torch.empty(cnt, dtype=torch.float64, device="cuda")
+    j = torch.empty(cnt, dtype=torch.int64, device="cuda")
+    assert lib.tsd_profile_merge_device(parts_c.data_ptr(), parts_j.data_ptr(), S, cnt, c.data_ptr(), j.data_ptr(),
+                                        st) == 0
+    assert lib.tsd_self_join_finish_device(d_t.data_ptr(), t.size, m, ctypes.c_size_t(-1).value, c.data_ptr(),
+                                           j.data_ptr(), st) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(j.cpu().numpy(), ref.indices) and np.array_equal(c.cpu().numpy(), ref.values)
+
+
+@pytest.mark.parametrize("nshards", [2, 5])
+def test_row_sharded_dictionary_join(nshards):
+    """row shards of a dictionary join (tsd_dict_shard_rows: whole 16384-window
+    reference blocks), joined one by one through the C ABI and concatenated,
+    reproduce the unsharded join (each shard has its own task decomposition,
+    so values agree to rounding; indices exactly up to ties) and the oracle"""
+    q = synth.walk(63, 5 * 16384 + 3000)
+    segs = list(synth.walks(64, 12, 700))
+    starts = [1000 * s for s in range(12)]
+    m = 150
+    D = _dict(segs, starts, m)
+    full = tsd.join_dictionary(q, D, m)
+    parts_v, parts_i = [], []
+    for s in range(nshards):
+        lo, hi = tsd.dict_shard_rows(q.size, m, s, nshards)
+        assert lo % 16384 == 0
+        if hi > lo:
+            P = tsd.join_dictionary(q[lo:hi + m - 1], D, m)
+            parts_v.append(P.values)
+            parts_i.append(P.indices)
+    v, i = np.concatenate(parts_v), np.concatenate(parts_i)
+    check_profile(v, i, full.values, full.indices, m, dict_dist(q, segs, starts, m), label=f"shards {nshards}")
+    rv, ri = O.dict_join(q, segs, starts, m)
+    check_profile(v, i, rv, ri, m, dict_dist(q, segs, starts, m), label=f"shards {nshards} vs oracle")
 
 
 @pytest.mark.parametrize("m", [2, 3])
