@@ -206,8 +206,11 @@ int plan_join_dev(tsd_dict_plan* p, const double* d_q, const size_t* q_len, size
   Error er{0, ""};
   JoinInputs in;
   int bad = -1;
-  TRY(compute_windows(d_q, N, m, groups, (int)nser, in.rows, ar, st, &bad, &er));
-  if (bad >= 0 || p->dict_nonfinite) return fail(kNonFiniteInput, "series contains a non-finite sample");
+  if (p->dict_nonfinite) return fail(kNonFiniteInput, "series contains a non-finite sample");
+  // the query's non-finite check is read after the join's final
+  // synchronisation (no host round trip between the statistics and the join)
+  const int* d_bad = nullptr;
+  TRY(compute_windows(d_q, N, m, groups, (int)nser, in.rows, ar, st, &bad, &er, &d_bad));
   in.xa = d_q;
   in.na = N;
   in.xb = p->d_xb;
@@ -235,6 +238,11 @@ int plan_join_dev(tsd_dict_plan* p, const double* d_q, const size_t* q_len, size
   launches += 3;
   CK(cudaEventRecord(p->s.ev[3], st));
   CK(cudaEventSynchronize(p->s.ev[3]));
+  {
+    int hb = 0x7fffffff;
+    CK(cudaMemcpy(&hb, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+    if (hb != 0x7fffffff) return fail(kNonFiniteInput, "series contains a non-finite sample");  // series.hpp:87
+  }
   float a = 0, b = 0;
   cudaEventElapsedTime(&a, p->s.ev[0], p->s.ev[3]);
   cudaEventElapsedTime(&b, p->s.ev[1], p->s.ev[2]);

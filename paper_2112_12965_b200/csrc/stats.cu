@@ -243,7 +243,8 @@ __global__ void k_window_stats(const double* __restrict__ x, const double2* __re
   } while (0)
 
 int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group>& groups, int nseries,
-                    WindowArrays& out, Arena& arena, cudaStream_t st, int* bad_series, Error* err) {
+                    WindowArrays& out, Arena& arena, cudaStream_t st, int* bad_series, Error* err,
+                    const int** d_bad_out) {
   (void)nseries;
   const int64_t nwin = n - m + 1;
   const int ng = (int)groups.size();
@@ -285,6 +286,11 @@ int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group
   k_window_stats<<<(unsigned)((nwin + 255) / 256), 256, 0, st>>>(d_x, d_P1, d_P2, nwin, m, d_groups, ng, d_gmax,
                                                                   out.mu, out.sd, out.invn, out.df, out.dg, out.flag);
   CUDA_TRY(cudaGetLastError());
+  if (d_bad_out) {  // the caller reads the non-finite flag after its own synchronisation
+    *d_bad_out = d_bad;
+    *bad_series = -1;
+    return kOk;
+  }
   int bad = big;
   CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));

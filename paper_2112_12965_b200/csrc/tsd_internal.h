@@ -93,8 +93,12 @@ bool device_free_bytes(size_t* free_bytes);
 // stats.cu -------------------------------------------------------------------
 // Computes window arrays for the concatenated buffer d_x[0..n). `bad_series`
 // receives (host) the lowest series index holding a non-finite sample, or -1.
+// d_bad_out != nullptr: no host synchronisation; *d_bad_out receives the device
+// int the caller reads after its own synchronisation (0x7fffffff = all
+// finite, else the lowest series index holding a non-finite sample).
 int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group>& groups, int nseries,
-                    WindowArrays& out, Arena& arena, cudaStream_t st, int* bad_series, Error* err);
+                    WindowArrays& out, Arena& arena, cudaStream_t st, int* bad_series, Error* err,
+                    const int** d_bad_out = nullptr);
 
 // join.cu --------------------------------------------------------------------
 struct JoinInputs {
