@@ -309,6 +309,7 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
     for (int r = 0; r < 16; ++r) v[r] = cmul(X[r], zbuf[j + 256 * r]);
     if (p + 1 < p1) fetch(p + 1);  // own entries only: no barrier needed
     fft4096<true>(v, fsm, j, stw);
+    TSD_CHECK(s0 >= 0 && s0 < a.nseg && s1 >= 0 && s1 < a.nseg + 1);
     double* h0 = a.heads + (int64_t)s0 * a.hstride;
     double* h1 = a.heads + (int64_t)s1 * a.hstride;
 #pragma unroll
@@ -316,6 +317,7 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
       const int q = j + 256 * r;
       const int64_t i = blk0 + q;
       if (q < a.Q && i < a.hrows) {
+        TSD_CHECK(i < a.hstride && (!two || s1 < a.nseg));
         const double d = dmu[q];
         const double g0 = v[r].x * invN - d * e0;
         h0[i] = g0;

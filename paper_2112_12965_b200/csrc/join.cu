@@ -118,6 +118,11 @@ struct JoinArgs {
   unsigned long long* ccand;     // [SYM_NC][ccols]: {order key of corr, row index} (16 B, 128-bit CAS)
   int64_t ccols;                 // columns per ccand copy
   double* cthr;                  // per column: kplus(best corr) * norm_b * (1 - 2^-40)
+  // buffer extents for TSD_CHECKED builds
+  int nseg_v;                    // virtual segments
+  int64_t hrows_alloc;           // heads rows allocated per segment (hstride)
+  int64_t tedge_rows;            // rows of the top-edge table
+  int nwarps_alloc;              // warps with edge / head scratch
 };
 
 template <int R>
@@ -356,6 +361,7 @@ __device__ __forceinline__ void fold_cmin(WarpSmem<R>& sm, int lane, int c) {
 template <int R>
 __device__ __forceinline__ void flush_block(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int b) {
   const int j = 32 * b + lane;
+  TSD_CHECK(b >= 0 && (b % 3) * 32 + lane < 96);
   if (j < cx.ncol - 1) cx.E[j] = sm.ering[(b % 3) * 32 + lane];
 }
 
@@ -449,6 +455,7 @@ __device__ __noinline__ void col_update(WarpSmem<R>& sm, int lane, unsigned cm, 
     const double t = kplus_d(key_value(wk)) * rcp_pos(invb) * (1.0 - 0x1p-40);
     atomicMax(reinterpret_cast<long long*>(cthr + col), __double_as_longlong(t));
     const int q = sm.cq_n;
+    TSD_CHECK(q < 40);
     sm.cq_key[q] = wk;
     sm.cq_row[q] = wrow;
     sm.cq_col[q] = col;
@@ -471,6 +478,7 @@ __device__ __noinline__ void col_flush(WarpSmem<R>& sm, int lane, unsigned long 
     unsigned long long* p = ccand;
     unsigned long long nk = 0, ni = 0, ck = 0, ci = 0;
     if (pend) {
+      TSD_CHECK(sm.cq_n <= 40 && sm.cq_col[e] >= 0);
       p = ccand + 2 * (long long)sm.cq_col[e];
       nk = sm.cq_key[e];
       ni = sm.cq_row[e];
@@ -1318,6 +1326,11 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_
         }
         const SegDev sg{sg0.col0 + q, sg0.src0 + q, sg0.ncol - q, 0};
         SweepCtx cx;
+        // column data (read in 32-column chunks, padded by 64) and this
+        // segment's edge slice (whole chunks) stay inside their buffers
+        TSD_CHECK(s >= 0 && s < a.nseg_v && gw < a.nwarps_alloc);
+        TSD_CHECK(sg.col0 >= 0 && sg.col0 + ((sg.ncol + 31) & ~31) <= a.ccols + 64);
+        TSD_CHECK(a.seg_eoff[s] + q + ((sg.ncol + 31) & ~31) <= a.ecap);
         cx.colg = a.col + sg.col0;
         cx.E = Ew + a.seg_eoff[s] + q;
         cx.ncol = sg.ncol;
@@ -1331,6 +1344,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_
         if (b == b0 && sg.ncol >= 2 && a.tedge) {
           // top edge precomputed by FFT correlation: E[q - delta] = cov(re, col0 + q)
           const int delta = i0 >= 1 ? 0 : 1;
+          TSD_CHECK(b0 / bpt < a.tedge_rows && sg.col0 + sg.ncol <= a.tstride);
           const double* te = a.tedge + (int64_t)(b0 / bpt) * a.tstride + sg.col0;
           for (int q = delta + lane; q < sg.ncol - 1 + delta; q += 32) {
             const double v = te[q] * (F32 ? a.scale[sg.col0 + q - delta] : 1.0);
@@ -1382,6 +1396,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_
             head[r] = out[r] - (mu - cA) * eU;
           }
         } else if (a.heads) {  // left edge precomputed by FFT correlation (heads_fft.cu)
+          TSD_CHECK(i0 + R * lane + R <= a.hstride && a.hstride <= a.hrows_alloc);
           const double2* hp = reinterpret_cast<const double2*>(a.heads + s * a.hstride + i0 + R * lane);
 #pragma unroll
           for (int r = 0; r < R / 2; ++r) {
@@ -1722,6 +1737,7 @@ __global__ void k_epilogue(const double* __restrict__ bc, const int64_t* __restr
     idx[o] = -1;
     return;
   }
+  TSD_CHECK(j < ncols);
   // concatenated column -> source coordinate (dictionary.hpp:183-188)
   int lo = 0, hi = nseg - 1, s = 0;
   while (lo <= hi) {
@@ -2340,6 +2356,10 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   a.seed = (d_heads || !SYM || (SELF && in.seed_corr && !F32)) ? d_seed : nullptr;
   a.tedge = d_te;
   a.tstride = tstride;
+  a.nseg_v = nseg;
+  a.hrows_alloc = hstride;
+  a.tedge_rows = d_te ? (nbands + bpt - 1) / bpt : 0;
+  a.nwarps_alloc = used_warps;
   a.tasks = d_tasks;
   a.task_next = d_tnext;
   a.ccand = d_ccand;

@@ -4,6 +4,26 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// TSD_CHECKED builds (tools/dev/abl_build.sh checked "-DTSD_CHECKED"): device
+// bounds assertions on the global and shared buffers the kernels index, the
+// stand-in for compute-sanitizer memcheck (closed on this GPU pool). A failed
+// check prints its site and traps; release builds compile them out.
+#ifdef TSD_CHECKED
+#include <cstdio>
+#define TSD_CHECK(cond)                                                                            \
+  do {                                                                                             \
+    if (!(cond)) {                                                                                 \
+      printf("TSD_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__,  \
+             (int)blockIdx.x, (int)threadIdx.x);                                                   \
+      __trap();                                                                                    \
+    }                                                                                              \
+  } while (0)
+#else
+#define TSD_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace tsd {
 
 // ---------------------------------------------------------------------------
