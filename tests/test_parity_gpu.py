@@ -696,10 +696,11 @@ def test_minimum_windows_all_joins(m):
     """the smallest windows (m = 2, 3): every pair is (nearly) perfectly
     correlated or anti-correlated -- ties and clamping everywhere.
 
-    Here the reference's own streaming correlation (QT - m mu_a mu_b over
-    sigma_a sigma_b, tsdict/src/join.cpp) is ill-conditioned: 2-sample windows
-    of a drifting walk have sigma ~1e-2 under means ~30, and its rho error
-    (~1e-8) exceeds the parity tolerance.  The exact answer is brute-force
+    Here the reference's own streaming correlation (the centred covariance
+    recurrence of profiles.hpp:288 / :330, normalised by invn_a invn_b at
+    :289 / :331) is ill-conditioned: 2-sample windows of a drifting walk have
+    sigma ~1e-2 under means ~30, and its rho error (~1e-8) exceeds the parity
+    tolerance.  The exact answer is brute-force
     per-pair z-normalisation, so the GPU is held to that at the standard
     tolerance, and the reference algorithm only to a conditioning bound."""
     a, b = synth.walk(81, 700), synth.walk(82, 500)
