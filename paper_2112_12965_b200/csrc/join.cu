@@ -35,6 +35,7 @@
 #include <queue>
 #include <cfloat>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -55,17 +56,31 @@ constexpr int TB = TSD_TB;  // threshold block (columns); nmin spans TB columns 
 #endif
 constexpr int WARPS = TSD_WARPS;  // warps per CTA (independent; small CTAs give finer occupancy steps)
 constexpr int T = 64;     // head / top-edge staging chunk (samples)
+// Register budgets. The default kernels take __launch_bounds__(64, MINB): with
+// MINB = 7 ptxas settles at 128 registers (a few bytes of call-site spills),
+// so 8 two-warp CTAs fit per SM at run time. TSD_NREG* > 0 instead caps the
+// registers with __maxnreg__ (the two qualifiers exclude each other): 144 ->
+// 7 CTAs (14 warps) per SM.
 #ifndef TSD_JOIN_MINB
-#define TSD_JOIN_MINB 7  // 7 two-warp CTAs per SM (the pipelined sweep needs ~140 registers; 8 CTAs spill)
+#define TSD_JOIN_MINB 7
 #endif
 #ifndef TSD_JOIN_MINB32
-#define TSD_JOIN_MINB32 7  // 7 CTAs: more registers for the 16-row FP32 lanes (C4 FP32 kernel 402 -> 388 ms)
+#define TSD_JOIN_MINB32 7
+#endif
+#ifndef TSD_JOIN_MINB_SYM
+#define TSD_JOIN_MINB_SYM 7
+#endif
+#ifndef TSD_NREG
+#define TSD_NREG 0     // FP64 AB / full-matrix sweep
+#endif
+#ifndef TSD_NREG32
+#define TSD_NREG32 0   // FP32 sweep
+#endif
+#ifndef TSD_NREG_SYM
+#define TSD_NREG_SYM 0  // symmetric self-join sweep
 #endif
 #ifndef TSD_PIPE
 #define TSD_PIPE 1  // the software-pipelined FP64 sweep (sweep_segment_p) for the AB / full-matrix joins
-#endif
-#ifndef TSD_JOIN_MINB_SYM
-#define TSD_JOIN_MINB_SYM 7  // the symmetric sweep's column side wants ~146 registers (7 CTAs: 2^21 self-join -2.6 %)
 #endif
 
 template <int R>
@@ -90,7 +105,7 @@ struct JoinArgs {
   const double* xb;
   const double* mub;
   const double4* col;   // column data (k_pack_cols / k_pack_cols32), padded by 64
-  const double* scale;  // s_j per concatenated column (FP32 normalised recurrence)
+  double f32_sig, f32_siga;  // FP32 sweep: cov scale sigma_a * sigma_b, row-data scale sigma_a (powers of 2)
   const SegDev* segs;
   const int* seg_eoff;  // compact edge offset of each segment inside its group (even)
   const double* btil;   // [nseg][m] centred samples of each segment's window 0
@@ -964,13 +979,20 @@ __device__ void sweep_segment_p(WarpSmem<R>& sm, const SweepCtx& cx, int lane, c
 }
 
 // ===========================================================================
-// FP32 mode: the same sweep with the column-normalised recurrence
-//   c~(i, k) = c~(i-1, k-1) * (s_k / s_{k-1}) + (df_a dg_b + dg_a df_b) * s_k,
-// s_k = invn_b[k], in packed fma.rn.f32x2 / mul.rn.f32x2 (FFMA2: two cells per
-// instruction). Window statistics, heads and top edges stay FP64 and are
-// rounded once; diagonals restart from an FP64 head at every segment start and
-// every task top, and tasks are capped at 4096 rows, which bounds the FP32
-// drift.
+// FP32 mode: the same sweep as FP64 in FP32 arithmetic -- the reference's
+// unnormalised centred recurrence cov = fma(dg_a, df_b, fma(df_a, dg_b, cov))
+// (profiles.hpp:330), two cells per fma.rn.f32x2 (FFMA2), 2 FP32 FMAs per
+// cell. The FP32 operands are the FP64 window statistics rounded once after a
+// power-of-two scaling (sigma_a for the query, sigma_b for the dictionary)
+// that brings the largest window norm of each side to ~1, so cov * sigma_a *
+// sigma_b stays inside the FP32 range; run_join falls back to the FP64 sweep
+// when the window norms span too wide a range for that (k_norm_range).
+// Heads and top edges stay FP64 and are rounded once; diagonals restart from
+// an FP64 head at every segment start and every task top, and tasks are capped
+// at 4096 rows, which bounds the FP32 drift. The rounding error
+// of a cell is that of the column-normalised form to first order (a column
+// scaling commutes with the relative rounding of each operation), at 2 instead
+// of 3 FP32 operations per cell.
 // A lane owns 16 consecutive rows (R = 16, bands of 512 rows). Physical
 // register pair q holds the slots (a, a + 8), a = (q - ph) mod 8: both halves
 // move down one slot per step in lockstep, so the rotation is pure register
@@ -978,6 +1000,9 @@ __device__ void sweep_segment_p(WarpSmem<R>& sm, const SweepCtx& cx, int lane, c
 // the slot-8 half takes the lane's own slot-7 value and the slot-0 half the
 // previous lane's slot-15 value (one 32-bit shuffle; lane 0 reads the band
 // above through the edge ring, lane 31's slot 15 is the band's bottom row).
+// Row test as in FP64: per 8-column block each slot's threshold is
+// kplus(best K) x the block's smallest scaled column norm (one FMUL2 per slot
+// pair), compared against the FP32 bits of cov with one ISETP per cell.
 // ===========================================================================
 typedef unsigned long long u64;
 
@@ -1001,18 +1026,21 @@ __device__ __forceinline__ float shfl_up1f(float v) {
   return v;
 }
 
-// FP32 column data, one 32-byte slot per column: {dg_b*s, dg_b*s, df_b*s,
-// df_b*s, s_k/s_{k-1}, s_k/s_{k-1}, invn_b/s, 0} (pairs pre-duplicated for f32x2)
+// FP32 column data, one 32-byte slot per column: {dg_b*sb, dg_b*sb, df_b*sb,
+// df_b*sb} (pairs pre-duplicated for f32x2), kf = invn_b / (sa*sb) (0 if
+// flat), nmin = (1 - 2^-20) x sa*sb x the smallest window norm over columns
+// j .. j+7 (flat or straddling: FLT_MAX) -- the block threshold factor
 struct __align__(16) Col32 {
-  u64 dg2, df2, rk2;
-  float kf, pad;
+  u64 dg2, df2;
+  float kf, nmin;
+  u64 pad;
 };
 static_assert(sizeof(Col32) == 32, "Col32 must match the double4 column slot");
 
-__device__ __forceinline__ int slot_thr32(float bK) { return bK > 0.0f ? __float_as_int(bK) : INT_MIN; }
+__device__ __forceinline__ float kplus_f(float b) { return b > 0.0f ? b : -0.0f; }
 
 struct StepIn32 {
-  u64 dg2, df2, rk2;
+  u64 dg2, df2;
   float e, in;
 };
 
@@ -1020,7 +1048,6 @@ __device__ __forceinline__ void prefetch32(const Col32* cb, const float* ep, flo
   const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(cb);
   d.dg2 = a.x;
   d.df2 = a.y;
-  d.rk2 = cb->rk2;
   d.e = *ep;
   d.in = shfl_up1f(v15);
 }
@@ -1029,19 +1056,31 @@ constexpr int R32 = 16;  // rows per lane in the FP32 sweep
 
 struct SweepState32 {
   u64 Q[8];       // physical pair q: slots ((q - ph) & 7, +8)
-  int thr[R32];   // slot_thr32(best K); the bests themselves live in sm.bK
+  u64 BK[8];      // kplus(best K) of slots (a, a + 8); the bests themselves live in sm.bK
+  float mbk;      // the smallest of the 16 kplus(best K): the lane threshold's factor
   StepIn32 nx;
-  bool dirty;     // some best changed in this block: refresh thr at its end
+  bool dirty;     // some best changed in this block: reload BK at its end
 };
 
-// warp vote over the 16 slot tests "bits(c~) >= thr" (four 4-deep predicate chains)
-__device__ __forceinline__ bool vote_any16f(const u64 (&Q)[8], int ph, const int (&thr)[R32]) {
-  int h[R32];
+__device__ __forceinline__ float min_bk16(const u64 (&BK)[8]) {
+  float m = fminf(lo2(BK[0]), hi2(BK[0]));
+#pragma unroll
+  for (int q = 1; q < 8; ++q) m = fminf(m, fminf(lo2(BK[q]), hi2(BK[q])));
+  return m;
+}
+
+// warp vote over the 16 slot tests "bits(cov) >= bits(thr)" (four 4-deep
+// predicate chains). A threshold from kplus(best) <= 0 is -0.0f (bits INT_MIN):
+// that slot passes everything
+__device__ __forceinline__ bool vote_any16f(const u64 (&Q)[8], int ph, const u64 (&TP)[8]) {
+  int h[R32], t[R32];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const int a = (q - ph + 8) & 7;  // slot order
     h[a] = (int)(unsigned)Q[q];
     h[a + 8] = (int)(unsigned)(Q[q] >> 32);
+    t[q] = (int)(unsigned)TP[q];
+    t[q + 8] = (int)(unsigned)(TP[q] >> 32);
   }
   unsigned r;
   asm volatile(
@@ -1057,11 +1096,36 @@ __device__ __forceinline__ bool vote_any16f(const u64 (&Q)[8], int ph, const int
       " vote.sync.any.pred a, a, -1;\n selp.u32 %0, 1, 0, a;\n}\n"
       : "=r"(r)
       : "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]), "r"(h[8]),
-        "r"(h[9]), "r"(h[10]), "r"(h[11]), "r"(h[12]), "r"(h[13]), "r"(h[14]), "r"(h[15]), "r"(thr[0]),
-        "r"(thr[1]), "r"(thr[2]), "r"(thr[3]), "r"(thr[4]), "r"(thr[5]), "r"(thr[6]), "r"(thr[7]), "r"(thr[8]),
-        "r"(thr[9]), "r"(thr[10]), "r"(thr[11]), "r"(thr[12]), "r"(thr[13]), "r"(thr[14]), "r"(thr[15]));
+        "r"(h[9]), "r"(h[10]), "r"(h[11]), "r"(h[12]), "r"(h[13]), "r"(h[14]), "r"(h[15]), "r"(t[0]),
+        "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(t[8]),
+        "r"(t[9]), "r"(t[10]), "r"(t[11]), "r"(t[12]), "r"(t[13]), "r"(t[14]), "r"(t[15]));
   return r != 0;
 }
+
+// First level of the FP32 row test (TSD_LANE_THR32): one threshold per lane,
+// kplus(the smallest of its 16 bests) x nmin, against the largest of the 16
+// slot values -- a VIMNMX3 tree instead of one ISETP per cell. As signed
+// integers the FP32 bit patterns order every non-negative value correctly
+// against a non-negative threshold and put any negative value below one; a
+// threshold of -0.0f (INT_MIN) passes everything. Only when some lane passes
+// does the warp run the 16 per-slot tests (vote_any16f), and only when one of
+// those passes, the exact update.
+__device__ __forceinline__ int max3i(int a, int b, int c) { return max(max(a, b), c); }
+__device__ __forceinline__ int min3i(int a, int b, int c) { return min(min(a, b), c); }
+__device__ __forceinline__ bool vote_lane16f(const u64 (&Q)[8], int thr) {
+  int h[16];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    h[2 * q] = (int)(unsigned)Q[q];
+    h[2 * q + 1] = (int)(unsigned)(Q[q] >> 32);
+  }
+  const int a = max3i(max3i(h[0], h[1], h[2]), max3i(h[3], h[4], h[5]), max3i(h[6], h[7], h[8]));
+  const int b = max3i(max3i(h[9], h[10], h[11]), max3i(h[12], h[13], h[14]), h[15]);
+  return __any_sync(0xffffffffu, a >= thr || b >= thr);
+}
+#ifndef TSD_LANE_THR32
+#define TSD_LANE_THR32 1
+#endif
 
 template <int R>
 __device__ __forceinline__ void issue_chunk32(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int c) {
@@ -1127,6 +1191,10 @@ __device__ __forceinline__ void sweep_block32(WarpSmem<R32>& sm, const SweepCtx&
   const int ebase = m96;
   float* const st_prev = sbase + (m96 == 0 ? 95 : m96 - 1);
   float* const st_cur = sbase + ebase;
+  // block thresholds: cov > best K / kf_j for some column j of the block
+  // implies cov > kplus(best K) x nmin (nmin lowered by 2^-20 for the rounding)
+  const float nm = ccur->nmin;
+  const int lthr = __float_as_int(S.mbk * nm);
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
     const int k = k0 + u;
@@ -1141,12 +1209,25 @@ __device__ __forceinline__ void sweep_block32(WarpSmem<R32>& sm, const SweepCtx&
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int a = (q - ph + 8) & 7;
-        const u64 t = fma2(FA[a], S.nx.dg2, mul2(GA[a], S.nx.df2));
-        S.Q[q] = fma2(S.Q[q], S.nx.rk2, t);
+        S.Q[q] = fma2(GA[a], S.nx.df2, fma2(FA[a], S.nx.dg2, S.Q[q]));  // profiles.hpp:330
       }
     }
     if (!GUARD || k + 1 < n) prefetch32(u + 1 < 8 ? ccur + u + 1 : cnext, &ring[ebase + u], hi2(S.Q[(ph + 7) & 7]), S.nx);
-    if (vote_any16f(S.Q, ph, S.thr)) [[unlikely]] {
+    // two-level test: the lane threshold (VIMNMX3 trees) first, the 16 slot
+    // thresholds only when some lane passes it
+    bool pass = TSD_LANE_THR32 ? vote_lane16f(S.Q, lthr) : true;
+    if (pass) [[unlikely]] {
+      u64 TP[8];
+      const u64 NM = pack2(nm, nm);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) TP[q] = mul2(S.BK[q], NM);
+      pass = vote_any16f(S.Q, ph, TP);
+    }
+    if (pass) [[unlikely]] {
+#ifdef TSD_COUNT_EXACT
+      if (lane == 0) atomicAdd(&g_exact_count, 1ull);
+      if (lane == 0 && cx.first_seg) atomicAdd(&g_exact_first, 1ull);
+#endif
       // stage the pairs in slot order and run the one shared exact update
       // (eight inline copies of it would overflow the instruction cache)
 #pragma unroll
@@ -1154,9 +1235,10 @@ __device__ __forceinline__ void sweep_block32(WarpSmem<R32>& sm, const SweepCtx&
       S.dirty |= exact_update32<SELF>(sm, lane, cx.colbase + k, (ccur + u)->kf, cx.row0, cx.excl);
     }
   }
-  if (S.dirty) {  // thresholds of the bests this block raised (stale ones only pass more cells)
+  if (S.dirty) {  // bests this block raised (the stale thresholds only passed more cells)
 #pragma unroll
-    for (int r = 0; r < R32; ++r) S.thr[r] = slot_thr32((float)sm.bK[r][lane]);
+    for (int q = 0; q < 8; ++q) S.BK[q] = pack2(kplus_f(sm.bK[q][lane]), kplus_f(sm.bK[q + 8][lane]));
+    S.mbk = min_bk16(S.BK);
     S.dirty = false;
   }
 }
@@ -1204,6 +1286,10 @@ __device__ void sweep_segment32(WarpSmem<R32>& sm, const SweepCtx& cx, int lane,
   }
   cp_wait<0>();
   __syncwarp();
+#ifdef TSD_COUNT_EXACT
+  if (lane == 0) atomicAdd(&g_step_count, (unsigned long long)n);
+  if (lane == 0 && cx.first_seg) atomicAdd(&g_step_first, (unsigned long long)n);
+#endif
   if (cx.write_out) {
     const int last = (n - 2) >> 5;
     for (int b = flushed; b <= last && n >= 2; ++b) flush_block32(sm, cx, lane, b);
@@ -1212,7 +1298,7 @@ __device__ void sweep_segment32(WarpSmem<R32>& sm, const SweepCtx& cx, int lane,
 }
 
 template <int R, bool SELF, bool F32, bool SYM>
-__global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_JOIN_MINB_SYM : TSD_JOIN_MINB) k_join(const JoinArgs a) {
+__device__ __forceinline__ void join_body(const JoinArgs& a) {
   static_assert(!SYM || (SELF && !F32), "the symmetric sweep is the FP64 self-join");
   constexpr int H = Geo<R>::H;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1347,7 +1433,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_
           TSD_CHECK(b0 / bpt < a.tedge_rows && sg.col0 + sg.ncol <= a.tstride);
           const double* te = a.tedge + (int64_t)(b0 / bpt) * a.tstride + sg.col0;
           for (int q = delta + lane; q < sg.ncol - 1 + delta; q += 32) {
-            const double v = te[q] * (F32 ? a.scale[sg.col0 + q - delta] : 1.0);
+            const double v = te[q] * (F32 ? a.f32_sig : 1.0);
             if constexpr (F32)
               reinterpret_cast<float*>(cx.E)[q - delta] = (float)v;
             else
@@ -1369,12 +1455,9 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_
 #pragma unroll
             for (int r = 0; r < R; ++r) {
               const int q = q0 + R * lane + r;
-              // delta = 1: row 0 adds nothing, so cov(0, q) = E[q-1]; FP32
-              // stores it in the scale of column q - delta (its consumer
-              // multiplies by s_k / s_{k-1})
+              // delta = 1: row 0 adds nothing, so cov(0, q) = E[q-1]
               if (q < sg.ncol - 1 + delta) {
-                const double v =
-                    (out[r] - (a.mub[sg.col0 + q] - cS) * eU) * (F32 ? a.scale[sg.col0 + q - delta] : 1.0);
+                const double v = (out[r] - (a.mub[sg.col0 + q] - cS) * eU) * (F32 ? a.f32_sig : 1.0);
                 if constexpr (F32)
                   reinterpret_cast<float*>(cx.E)[q - delta] = (float)v;
                 else
@@ -1404,10 +1487,9 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_
             head[2 * r] = h2.x;
             head[2 * r + 1] = h2.y;
           }
-          if constexpr (F32) {  // the FP32 sweep runs the column-normalised recurrence
-            const double s0 = a.scale[sg.col0];
+          if constexpr (F32) {  // the FP32 sweep's scaled covariances
 #pragma unroll
-            for (int r = 0; r < R; ++r) head[r] *= s0;
+            for (int r = 0; r < R; ++r) head[r] *= a.f32_sig;
           }
         } else {  // left edge: cov(i, col0) for the band's rows, batched 8 segments at a time
 #ifndef TSD_ABL_NOHEADS
@@ -1425,7 +1507,7 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_
           } else {
             sliding_dot<R>(sm, a.btil + (int64_t)s * a.m, 0.0, a.xa + i0, a.na - i0, cA, a.m, lane, out, nullptr);
           }
-          const double e = a.ebt[s], s0 = F32 ? a.scale[sg.col0] : 1.0;
+          const double e = a.ebt[s], s0 = F32 ? a.f32_sig : 1.0;
 #pragma unroll
           for (int r = 0; r < R; ++r) {
             const int64_t i = i0 + R * lane + r;
@@ -1441,24 +1523,23 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_
           for (int r = 0; r < R; ++r) {
             const int64_t i = i0 + R * lane + r;
             const bool in = i < a.nrows;
-            fa[r] = in ? (float)a.dfa[i] : 0.0f;
-            ga[r] = in ? (float)a.dga[i] : 0.0f;
+            fa[r] = in ? (float)(a.dfa[i] * a.f32_siga) : 0.0f;
+            ga[r] = in ? (float)(a.dga[i] * a.f32_siga) : 0.0f;
           }
           u64 FA[8], GA[8];
-          SweepState32 S;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             FA[q] = pack2(fa[q], fa[q + 8]);
             GA[q] = pack2(ga[q], ga[q + 8]);
-            S.Q[q] = pack2((float)head[q], (float)head[q + 8]);
           }
           // bests as FP32 values (seeds rounded once; +inf = inactive row)
+          SweepState32 S;
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const float bk = (float)sm.bK[r][lane];
-            sm.bK[r][lane] = (double)bk;
-            S.thr[r] = slot_thr32(bk);
+          for (int q = 0; q < 8; ++q) {
+            S.Q[q] = pack2((float)head[q], (float)head[q + 8]);
+            S.BK[q] = pack2(kplus_f(sm.bK[q][lane]), kplus_f(sm.bK[q + 8][lane]));
           }
+          S.mbk = min_bk16(S.BK);
           S.dirty = false;
           if constexpr (R == R32) sweep_segment32<SELF>(sm, cx, lane, FA, GA, S);
         } else if (TSD_PIPE && !SYM) {
@@ -1527,6 +1608,21 @@ __global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_
   }
 }
 
+template <int R, bool SELF, bool F32, bool SYM>
+constexpr int join_nreg() {
+  return F32 ? TSD_NREG32 : SYM ? TSD_NREG_SYM : TSD_NREG;
+}
+// two kernels around one body: the launch-bound budget, or a __maxnreg__ cap
+template <int R, bool SELF, bool F32, bool SYM>
+__global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_JOIN_MINB_SYM : TSD_JOIN_MINB)
+    k_join(const JoinArgs a) {
+  join_body<R, SELF, F32, SYM>(a);
+}
+template <int R, bool SELF, bool F32, bool SYM>
+__global__ void __maxnreg__((join_nreg<R, SELF, F32, SYM>() > 0 ? join_nreg<R, SELF, F32, SYM>() : 128)) k_join_wide(const JoinArgs a) {
+  join_body<R, SELF, F32, SYM>(a);
+}
+
 // centred top window of each band range (row re = first row - 1, or 0 for
 // the first range): w[r][k] = x[re + k] - mu[re], e[r] = sum_k w[r][k]
 __global__ void k_topwin(const double* __restrict__ x, const double* __restrict__ mu, int nbr, int rows_per_range,
@@ -1574,15 +1670,14 @@ __global__ void k_merge_groups(double* __restrict__ c, int64_t* __restrict__ j, 
 // with nmin = (1 - 2^-40) x the smallest window norm 1/invn_b over windows
 // j .. j+TB-1 (flat or straddling windows count as DBL_MAX): the block
 // threshold of the sweep, whose blocks start at multiples of TB of a
-// segment's columns. scale[j] (s_j = invn_b, 1 if flat) serves the FP32 path.
+// segment's columns.
 __global__ void k_pack_cols(const double* __restrict__ df, const double* __restrict__ dg,
                             const double* __restrict__ invn, const uint8_t* __restrict__ flag, int64_t n,
-                            double4* __restrict__ col, double* __restrict__ scale) {
+                            double4* __restrict__ col) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n + 64) return;
   if (i >= n) {
     col[i] = make_double4(0, 0, 0, DBL_MAX);
-    scale[i] = 1.0;
     return;
   }
   double nm = DBL_MAX;
@@ -1592,34 +1687,60 @@ __global__ void k_pack_cols(const double* __restrict__ df, const double* __restr
   }
   const double iv = invn[i];
   col[i] = make_double4(df[i], dg[i], iv, nm < DBL_MAX ? nm * (1.0 - 0x1p-40) : DBL_MAX);
-  scale[i] = iv > 0.0 ? iv : 1.0;
 }
 
 // FP32 column data (Col32 layout in the same 32-byte slots), from FP64 values
+// scaled by sigma_b (column data) and sigma = sigma_a * sigma_b (covariances);
+// nmin over the 8-column threshold block (TB = 8 in the FP32 sweep)
 __global__ void k_pack_cols32(const double* __restrict__ df, const double* __restrict__ dg,
-                              const double* __restrict__ invn, int64_t n, double4* __restrict__ col,
-                              double* __restrict__ scale) {
+                              const double* __restrict__ invn, const uint8_t* __restrict__ flag, int64_t n,
+                              double4* __restrict__ col, double sigb, double sig) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n + 64) return;
   Col32 c;
+  c.pad = 0;
   if (i >= n) {
     c.dg2 = c.df2 = 0;
-    c.rk2 = pack2(1.0f, 1.0f);
     c.kf = 0.0f;
+    c.nmin = FLT_MAX;
   } else {
+    double nm = DBL_MAX;
+    for (int t = 0; t < 8 && i + t < n; ++t) {
+      const double iv = invn[i + t];
+      if ((flag[i + t] & 1) && iv > 0.0) nm = fmin(nm, 1.0 / iv);
+    }
     const double iv = invn[i];
-    const double sj = iv > 0.0 ? iv : 1.0;
-    const double ivp = i > 0 ? invn[i - 1] : 0.0;
-    const double sp = ivp > 0.0 ? ivp : 1.0;
-    const float g = (float)(dg[i] * sj), f = (float)(df[i] * sj), r = (float)(sj / sp);
+    const float g = (float)(dg[i] * sigb), f = (float)(df[i] * sigb);
     c.dg2 = pack2(g, g);
     c.df2 = pack2(f, f);
-    c.rk2 = pack2(r, r);
-    c.kf = iv > 0.0 ? 1.0f : 0.0f;
-    scale[i] = sj;
+    c.kf = iv > 0.0 ? (float)(iv / sig) : 0.0f;
+    c.nmin = nm < DBL_MAX ? (float)(nm * sig * (1.0 - 0x1p-20)) : FLT_MAX;
   }
-  c.pad = 0.0f;
   reinterpret_cast<Col32*>(col)[i] = c;
+}
+
+// smallest and largest window norm over valid non-flat windows, as positive
+// double bits (order-preserving as integers): out[0] = min, out[1] = max
+__global__ void k_norm_range(const double* __restrict__ invn, const uint8_t* __restrict__ flag, int64_t n,
+                             unsigned long long* __restrict__ out) {
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double iv = invn[i];
+    if (flag[i] == 1 && iv > 0.0) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(1.0 / iv);
+      lo = min(lo, b);
+      hi = max(hi, b);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, lo);
+    atomicMax(out + 1, hi);
+  }
 }
 
 __global__ void k_btil(const double* __restrict__ xb, const double* __restrict__ mub, const SegDev* __restrict__ segs,
@@ -1965,7 +2086,12 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem_bytes = sizeof(WarpSmem<R>) * WARPS;
-  auto kern = k_join<R, SELF, F32, SYM>;
+  auto kern = [] {
+    if constexpr (join_nreg<R, SELF, F32, SYM>() == 0)
+      return k_join<R, SELF, F32, SYM>;
+    else
+      return k_join_wide<R, SELF, F32, SYM>;
+  }();
   vmark("segments");
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes));
   int occ = 0;
@@ -2189,7 +2315,6 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   int* d_eoff = (int*)arena.get(sizeof(int) * nseg);
   int* d_gs = (int*)arena.get(sizeof(int) * (G + 1));
   double4* d_col = (double4*)arena.get(sizeof(double4) * (in.cols.nwin + 64));
-  double* d_scale = (double*)arena.get(sizeof(double) * (in.cols.nwin + 64));
   double* d_btil = (double*)arena.get(sizeof(double) * (int64_t)nseg * m);
   double* d_ebt = (double*)arena.get(sizeof(double) * nseg);
   double* d_edges = (double*)arena.get(sizeof(double) * ecap * used_warps);
@@ -2222,7 +2347,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     // partial rows must read "no candidate" in the merge
     CUDA_TRY(cudaMemsetAsync(d_pj, 0xff, sizeof(int64_t) * nrows * G, st));
   }
-  if (!d_segs || !d_eoff || !d_gs || !d_col || !d_scale || !d_hscr || !d_btil || !d_ebt || !d_edges || !d_pc || !d_pj) {
+  if (!d_segs || !d_eoff || !d_gs || !d_col || !d_hscr || !d_btil || !d_ebt || !d_edges || !d_pc || !d_pj) {
     if (err) *err = Error{kCudaError, "device allocation failed for the join"};
     return kCudaError;
   }
@@ -2231,11 +2356,12 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   CUDA_TRY(cudaMemcpyAsync(d_gs, group_seg.data(), sizeof(int) * (G + 1), cudaMemcpyHostToDevice, st));
   int nl = 0;
   if (F32)
-    k_pack_cols32<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(in.cols.df, in.cols.dg, in.cols.invn,
-                                                                              in.cols.nwin, d_col, d_scale);
+    k_pack_cols32<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(
+        in.cols.df, in.cols.dg, in.cols.invn, in.cols.flag, in.cols.nwin, d_col, in.f32_sigb,
+        in.f32_siga * in.f32_sigb);
   else
     k_pack_cols<<<(unsigned)((in.cols.nwin + 64 + 255) / 256), 256, 0, st>>>(
-        in.cols.df, in.cols.dg, in.cols.invn, in.cols.flag, in.cols.nwin, d_col, d_scale);
+        in.cols.df, in.cols.dg, in.cols.invn, in.cols.flag, in.cols.nwin, d_col);
   ++nl;
   k_btil<<<nseg, 128, 0, st>>>(in.xb, in.cols.mu, d_segs, m, d_btil, d_ebt);
   ++nl;
@@ -2311,7 +2437,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   a.xb = in.xb;
   a.mub = in.cols.mu;
   a.col = d_col;
-  a.scale = d_scale;
+  a.f32_sig = in.f32_siga * in.f32_sigb;
+  a.f32_siga = in.f32_siga;
   a.segs = d_segs;
   a.seg_eoff = d_eoff;
   a.btil = d_btil;
@@ -2458,8 +2585,51 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
              int* launches) {
   const bool self = in.excl >= 0;
   if (in.precision == 1) {
-    const int rc = self ? launch_join<R32, true, true, false>(in, d_best_c, d_best_j, arena, st, err, launches)
-                        : launch_join<R32, false, true, false>(in, d_best_c, d_best_j, arena, st, err, launches);
+    // power-of-two scalings that bring the largest window norm of each side
+    // to (1/2, 1]: every scaled covariance then lies in [-1, 1]. The FP32
+    // sweep needs the smallest scaled products (and the K = cov * invn_b
+    // values) to stay well inside the FP32 range; inputs whose window norms
+    // span more than that (about 2^96 over both sides -- e.g. blocks of the
+    // query at wildly different magnitudes) run the FP64 sweep instead.
+    unsigned long long* d_rng = (unsigned long long*)arena.get(sizeof(unsigned long long) * 4);
+    if (!d_rng) {
+      if (err) *err = Error{kCudaError, "device allocation failed for the FP32 scaling"};
+      return kCudaError;
+    }
+    const unsigned long long init[4] = {~0ull, 0ull, ~0ull, 0ull};
+    CUDA_TRY(cudaMemcpyAsync(d_rng, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    k_norm_range<<<296, 256, 0, st>>>(in.rows.invn, in.rows.flag, in.rows.nwin, d_rng);
+    k_norm_range<<<296, 256, 0, st>>>(in.cols.invn, in.cols.flag, in.cols.nwin, d_rng + 2);
+    if (launches) *launches += 2;
+    unsigned long long rng[4];
+    CUDA_TRY(cudaMemcpyAsync(rng, d_rng, sizeof(rng), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    auto side = [](unsigned long long lo, unsigned long long hi, double& mn, double& mx) {
+      if (hi == 0) {  // no non-flat window: nothing to scale
+        mn = mx = 1.0;
+        return;
+      }
+      mn = __builtin_bit_cast(double, lo);
+      mx = __builtin_bit_cast(double, hi);
+    };
+    double mna, mxa, mnb, mxb;
+    side(rng[0], rng[1], mna, mxa);
+    side(rng[2], rng[3], mnb, mxb);
+    JoinInputs fin = in;
+    fin.f32_siga = std::ldexp(1.0, -std::ilogb(mxa) - 1);
+    fin.f32_sigb = std::ldexp(1.0, -std::ilogb(mxb) - 1);
+    const double span = (mna / mxa) * (mnb / mxb);
+    const bool fits = span > 0x1p-96 && mxa < 0x1p100 && mxa * (mxb / mnb) < 0x1p110;
+    if (getenv("TSD_VERBOSE"))
+      fprintf(stderr, "[tsd] fp32 norms a [%.3g, %.3g] b [%.3g, %.3g] -> %s\n", mna, mxa, mnb, mxb,
+              fits ? "fp32 sweep" : "fp64 sweep (norm range too wide for fp32)");
+    if (!fits) {
+      JoinInputs din = in;
+      din.precision = 0;
+      return run_join(din, d_best_c, d_best_j, arena, st, err, launches);
+    }
+    const int rc = self ? launch_join<R32, true, true, false>(fin, d_best_c, d_best_j, arena, st, err, launches)
+                        : launch_join<R32, false, true, false>(fin, d_best_c, d_best_j, arena, st, err, launches);
     if (rc != kOk) return rc;
     const int64_t n = in.rows.nwin;
     k_refine_fp64<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_best_c, d_best_j, n, in.xa, in.rows.mu,

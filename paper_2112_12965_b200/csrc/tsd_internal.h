@@ -125,6 +125,8 @@ struct JoinInputs {
   // starts each row at (bound - seed_margin)
   const double* seed_corr = nullptr;
   double seed_margin = 0.0;
+  // FP32 sweep: power-of-two scalings of the query / dictionary statistics (run_join)
+  double f32_siga = 1.0, f32_sigb = 1.0;
 };
 
 // Runs the row-band join of every row against every valid column of every
