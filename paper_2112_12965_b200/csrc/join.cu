@@ -827,15 +827,38 @@ struct PipeState {
   double PA[R], PB[R];  // column values: even columns in PA, odd in PB
   double bKp[R];        // kplus(bestK)
   int thr[R];           // hi(bKp * nmin) of the current threshold block
+  int lthr;             // TSD_LANE_THR64: the smallest of thr (the lane threshold)
   double dfb, dgb, e, in, nmin;  // prefetched column data / incoming diagonals of the next column
   bool dirty;
 };
+
+#ifndef TSD_LANE_THR64
+#define TSD_LANE_THR64 1
+#endif
+// first level of the FP64 row test (TSD_LANE_THR64): the largest high word of
+// the lane's 8 values against the smallest slot threshold (VIMNMX3 tree);
+// the 8 per-slot tests run only when some lane passes it. High words of
+// doubles order like the FP32 bit patterns of vote_lane16f (sign included).
+__device__ __forceinline__ bool vote_lane8(const double (&V)[8], int thr) {
+  int h[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) h[r] = __double2hiint(V[r]);
+  const int a = max(max(h[0], h[1]), h[2]), b = max(max(h[3], h[4]), h[5]);
+  return __any_sync(0xffffffffu, max(max(a, b), max(h[6], h[7])) >= thr);
+}
+__device__ __forceinline__ int min_thr8(const int (&t)[8]) {
+  return min(min(min(t[0], t[1]), t[2]), min(min(min(t[3], t[4]), t[5]), min(t[6], t[7])));
+}
 
 // the high-word test of the column held in V (column c = k0 + uc, ring
 // position of its column data pos), then the exact update on a pass
 template <int R, bool SELF>
 __device__ __forceinline__ void pipe_test(WarpSmem<R>& sm, const SweepCtx& cx, int lane, PipeState<R>& S,
                                           const double (&V)[R], int c, int pos) {
+  // (AB / dictionary joins only: the self-join's near-periodic candidates pass
+  // the lane threshold too often -- C2 5.07 -> 5.15 ms with it, C4 539 -> 527 ms)
+  if (TSD_LANE_THR64 && !SELF && !vote_lane8(V, S.lthr)) [[likely]]
+    return;
   if (vote_any8(V, 0, S.thr)) [[unlikely]] {
 #ifdef TSD_COUNT_EXACT
     if (lane == 0) atomicAdd(&g_exact_count, 1ull);
@@ -875,6 +898,7 @@ __device__ __forceinline__ void sweep_block_p(WarpSmem<R>& sm, const SweepCtx& c
       S.nmin = ccur[0].w;
 #pragma unroll
       for (int r = 0; r < R; ++r) S.thr[r] = __double2hiint(S.bKp[r] * S.nmin);
+      S.lthr = min_thr8(S.thr);
     } else {
       // column k from column k - 1: slots 7..1 first (slot 7 feeds the next shuffle)
 #pragma unroll
@@ -911,6 +935,7 @@ __device__ __forceinline__ void sweep_block_p(WarpSmem<R>& sm, const SweepCtx& c
         }
 #pragma unroll
         for (int r = 0; r < R; ++r) S.thr[r] = __double2hiint(S.bKp[r] * S.nmin);
+        S.lthr = min_thr8(S.thr);
       }
     }
   }
@@ -1111,7 +1136,6 @@ __device__ __forceinline__ bool vote_any16f(const u64 (&Q)[8], int ph, const u64
 // does the warp run the 16 per-slot tests (vote_any16f), and only when one of
 // those passes, the exact update.
 __device__ __forceinline__ int max3i(int a, int b, int c) { return max(max(a, b), c); }
-__device__ __forceinline__ int min3i(int a, int b, int c) { return min(min(a, b), c); }
 __device__ __forceinline__ bool vote_lane16f(const u64 (&Q)[8], int thr) {
   int h[16];
 #pragma unroll
@@ -2085,7 +2109,10 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const size_t smem_bytes = sizeof(WarpSmem<R>) * WARPS;
+  // TSD_SMEM_PAD (development): extra dynamic shared memory per CTA, to probe the
+  // sweep's sensitivity to resident warps
+  static const size_t smem_pad = getenv("TSD_SMEM_PAD") ? (size_t)atol(getenv("TSD_SMEM_PAD")) : 0;
+  const size_t smem_bytes = sizeof(WarpSmem<R>) * WARPS + smem_pad;
   auto kern = [] {
     if constexpr (join_nreg<R, SELF, F32, SYM>() == 0)
       return k_join<R, SELF, F32, SYM>;
