@@ -2646,7 +2646,8 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     fin.f32_siga = std::ldexp(1.0, -std::ilogb(mxa) - 1);
     fin.f32_sigb = std::ldexp(1.0, -std::ilogb(mxb) - 1);
     const double span = (mna / mxa) * (mnb / mxb);
-    const bool fits = span > 0x1p-96 && mxa < 0x1p100 && mxa * (mxb / mnb) < 0x1p110;
+    // (K = cov * invn_b, bounded by mxa * mxb / mnb, is kept in FP32 too)
+    const bool fits = span > 0x1p-96 && mxa * (mxb / mnb) < 0x1p110;
     if (getenv("TSD_VERBOSE"))
       fprintf(stderr, "[tsd] fp32 norms a [%.3g, %.3g] b [%.3g, %.3g] -> %s\n", mna, mxa, mnb, mxb,
               fits ? "fp32 sweep" : "fp64 sweep (norm range too wide for fp32)");

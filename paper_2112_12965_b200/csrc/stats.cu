@@ -75,8 +75,12 @@ __device__ __forceinline__ dd2 shfl_up_dd2(const dd2& v, int d) {
   return r;
 }
 
-// block-wide inclusive scan of one dd2 per thread; returns inclusive value
-__device__ dd2 block_scan(dd2 v, dd2* sh_warp) {
+// block-wide scan of one dd2 per thread; returns the EXCLUSIVE prefix (the
+// sum over the lower threads), formed by shifting the inclusive scan one lane
+// rather than as inclusive - own: a thread whose own sum dwarfs everything
+// before it (a 1e60 excursion after 1e-6 data) would cancel the earlier
+// prefix away. *total (thread 0's copy valid after the call) = block sum.
+__device__ dd2 block_scan_excl(dd2 v, dd2* sh_warp, dd2* total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int o = 1; o < 32; o <<= 1) {
     dd2 u = shfl_up_dd2(v, o);
@@ -94,8 +98,11 @@ __device__ dd2 block_scan(dd2 v, dd2* sh_warp) {
     if (lane < nw) sh_warp[lane] = w;
   }
   __syncthreads();
-  if (wid > 0) v = dd2_add(sh_warp[wid - 1], v);
-  return v;
+  dd2 ex = shfl_up_dd2(v, 1);  // inclusive of the lane below, within the warp
+  if (lane == 0) ex = dd2{{0, 0}, {0, 0}};
+  if (wid > 0) ex = dd2_add(sh_warp[wid - 1], ex);
+  if (total) *total = sh_warp[(blockDim.x >> 5) - 1];
+  return ex;
 }
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_partial(const double* __restrict__ x, int64_t n,
@@ -110,8 +117,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_partial(const double* __r
     acc.a = dd_add(acc.a, a);
     acc.b = dd_add(acc.b, b);
   }
-  dd2 inc = block_scan(acc, sh);
-  if (threadIdx.x == blockDim.x - 1) block_sums[blockIdx.x] = inc;
+  dd2 tot;
+  block_scan_excl(acc, sh, &tot);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = tot;
 }
 
 // exclusive scan of nblocks block sums in place, one CTA of 1024 threads
@@ -122,11 +130,8 @@ __global__ void __launch_bounds__(1024) k_scan_blocks(dd2* __restrict__ sums, in
   dd2 acc{{0, 0}, {0, 0}};
   for (int64_t k = 0; k < per; ++k)
     if (b0 + k < nblocks) acc = dd2_add(acc, sums[b0 + k]);
-  dd2 inc = block_scan(acc, sh);
   // exclusive prefix for this thread's range
-  dd2 run{{inc.a.hi, inc.a.lo}, {inc.b.hi, inc.b.lo}};
-  run.a = dd_sub(run.a, acc.a);
-  run.b = dd_sub(run.b, acc.b);
+  dd2 run = block_scan_excl(acc, sh, nullptr);
   __syncthreads();
   for (int64_t k = 0; k < per; ++k) {
     if (b0 + k < nblocks) {
@@ -150,10 +155,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const double* __res
     acc.a = dd_add(acc.a, a);
     acc.b = dd_add(acc.b, b);
   }
-  dd2 inc = block_scan(acc, sh);
-  dd2 run = dd2_add(block_excl[blockIdx.x], inc);
-  run.a = dd_sub(run.a, acc.a);
-  run.b = dd_sub(run.b, acc.b);
+  dd2 run = dd2_add(block_excl[blockIdx.x], block_scan_excl(acc, sh, nullptr));
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     P1[0] = make_double2(0.0, 0.0);
     P2[0] = make_double2(0.0, 0.0);
@@ -170,8 +172,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const double* __res
   }
 }
 
-__device__ __forceinline__ void window_moments(const double2* __restrict__ P1, const double2* __restrict__ P2,
-                                               int64_t p, int m, double& mean, double& var) {
+// Window mean and variance from the double-double prefix sums. Their
+// differences carry an absolute error of about 2^-100 x the prefix
+// magnitude; when that threatens the variance's twelfth digit (a quiet
+// window after a huge excursion somewhere earlier in the buffer) the window
+// is redone in two compensated passes over its samples, as the reference
+// does for its Kahan prefix sums (series.hpp:126-142).
+__device__ __forceinline__ void window_moments(const double* __restrict__ x, const double2* __restrict__ P1,
+                                               const double2* __restrict__ P2, int64_t p, int m, double& mean,
+                                               double& var) {
   const double md = (double)m;
   const double2 a0 = P1[p], a1 = P1[p + m], b0 = P2[p], b1 = P2[p + m];
   const dd w1 = dd_sub(dd{a1.x, a1.y}, dd{a0.x, a0.y});
@@ -181,6 +190,23 @@ __device__ __forceinline__ void window_moments(const double2* __restrict__ P1, c
   mean = mu.hi + mu.lo;
   var = v.hi + v.lo;
   if (var < 0.0) var = 0.0;
+  const double e2 = 0x1p-100 * (fabs(b1.x) + fabs(b0.x));                // error of w2
+  const double e1 = 0x1p-100 * (fabs(a1.x) + fabs(a0.x));                // error of w1
+  if (e2 > 1e-12 * md * var || e1 * e1 > 1e-24 * md * md * var) [[unlikely]] {
+    dd s{0.0, 0.0};
+    for (int t = 0; t < m; ++t) s = dd_add(s, dd{x[p + t], 0.0});
+    const dd mu2 = dd_div_d(s, md);
+    const double mc = mu2.hi + mu2.lo;
+    dd q{0.0, 0.0};
+    for (int t = 0; t < m; ++t) {
+      const dd d = dd_sub(dd{x[p + t], 0.0}, mu2);
+      q = dd_add(q, dd_mul(d, d));
+    }
+    const dd v2 = dd_div_d(q, md);
+    mean = mc;
+    var = v2.hi + v2.lo;
+    if (var < 0.0) var = 0.0;
+  }
 }
 
 __global__ void k_window_stats(const double* __restrict__ x, const double2* __restrict__ P1,
@@ -192,7 +218,7 @@ __global__ void k_window_stats(const double* __restrict__ x, const double2* __re
   if (p >= nwin) return;
   const double md = (double)m;
   double mean, var;
-  window_moments(P1, P2, p, m, mean, var);
+  window_moments(x, P1, P2, p, m, mean, var);
   const double sd = sqrt(var);
   // group lookup: last group with wbeg <= p
   int lo = 0, hi = ngroups - 1, g = -1;
@@ -222,7 +248,7 @@ __global__ void k_window_stats(const double* __restrict__ x, const double2* __re
   double dfv = 0.0, dgv = 0.0;
   if (p > 0) {
     double mean_prev, var_prev;
-    window_moments(P1, P2, p - 1, m, mean_prev, var_prev);
+    window_moments(x, P1, P2, p - 1, m, mean_prev, var_prev);
     const double xin = x[p + m - 1], xout = x[p - 1];
     dfv = 0.5 * (xin - xout);
     dgv = (xin - mean) + (xout - mean_prev);

@@ -477,6 +477,68 @@ def test_fp32_mode_self_join_and_flat():
     check_profile(P.values, P.indices, rv, ri, 64, ab_dist(a, b, 64), fp32=True, label="fp32 flat")
 
 
+def test_fp32_scaling_and_fp64_fallback(capfd, monkeypatch):
+    """The FP32 sweep runs on power-of-two scaled statistics (join.cu
+    run_join): inputs at extreme but uniform magnitudes stay in FP32; a query
+    whose window norms span more than the FP32 range (two 16384-window blocks
+    at 1e-6 and 1e60 -- each non-flat against its own block maximum,
+    dictionary.hpp:175-180) runs the FP64 sweep instead. Both within the
+    FP32 tolerance of the oracle."""
+    monkeypatch.setenv("TSD_VERBOSE", "1")
+    m = 128
+    segs = [synth.walk(90 + k, 1500) for k in range(4)]
+    starts = [3000 * k for k in range(4)]
+    # uniform extreme magnitudes: the FP32 sweep with sigma_a ~ 2^-90, sigma_b ~ 2^7
+    q = 1e25 * synth.walk(95, 30000)
+    segs_s = [1e-3 * s for s in segs]
+    capfd.readouterr()
+    P = tsd.join_dictionary(q, _dict(segs_s, starts, m), m, precision="fp32")
+    err = capfd.readouterr().err
+    assert "-> fp32 sweep" in err, err[-2000:]
+    rv, ri = O.dict_join(q, segs_s, starts, m)
+    st = check_profile(P.values, P.indices, rv, ri, m, dict_dist(q, segs_s, starts, m), fp32=True,
+                       label="fp32 extreme uniform magnitudes")
+    assert st["max_abs"] <= 1e-3
+    # norms spanning ~1e66 across query blocks: FP64 fallback
+    q2 = synth.walk(96, 40000)
+    q2[:20000] *= 1e-6
+    q2[20000:] *= 1e60
+    capfd.readouterr()
+    P = tsd.join_dictionary(q2, _dict(segs, starts, m), m, precision="fp32")
+    err = capfd.readouterr().err
+    assert "fp64 sweep (norm range too wide" in err, err[-2000:]
+    rv, ri = O.dict_join(q2, segs, starts, m)
+    st = check_profile(P.values, P.indices, rv, ri, m, dict_dist(q2, segs, starts, m), fp32=True,
+                       label="fp32 -> fp64 fallback")
+    assert st["max_abs"] <= 1e-3
+
+
+@pytest.mark.parametrize("order", ["quiet_then_huge", "huge_then_quiet"])
+def test_window_stats_and_join_across_huge_excursions(order):
+    """Window statistics over one buffer holding 1e-6-scale and 1e60-scale
+    stretches (stats.cu): the scans' exclusive prefixes must not cancel the
+    quiet prefix against a huge block sum, and quiet windows AFTER the huge
+    stretch -- which the double-double prefix differences cannot resolve --
+    take the two-pass fallback (series.hpp:126-142). Statistics against the
+    oracle (1e-9, flat mask identical), then the FP64 dictionary join."""
+    m = 128
+    x = synth.walk(97, 40000)
+    lo, hi = (slice(0, 20000), slice(20000, None)) if order == "quiet_then_huge" else (slice(20000, None), slice(0, 20000))
+    x[lo] *= 1e-6
+    x[hi] *= 1e60
+    st = tsd.compute_stats(x, m)
+    mu, sd, _, flat = O.compute_stats(x, m)
+    assert np.array_equal(st.constant_mask.astype(bool), np.asarray(flat).astype(bool))
+    assert np.max(np.abs(st.means - mu) / np.maximum(np.abs(mu), 1e-300)) < 1e-9
+    nz = np.asarray(sd) > 0
+    assert np.max(np.abs(st.stds[nz] - sd[nz]) / sd[nz]) < 1e-9
+    segs = [synth.walk(90 + k, 1500) for k in range(4)]
+    starts = [3000 * k for k in range(4)]
+    P = tsd.join_dictionary(x, _dict(segs, starts, m), m)
+    rv, ri = O.dict_join(x, segs, starts, m)
+    check_profile(P.values, P.indices, rv, ri, m, dict_dist(x, segs, starts, m), label=f"excursions {order}")
+
+
 @pytest.mark.parametrize("nq", [64 + 1, 64 + 7, 64 + 511, 64 + 512, 64 + 513, 64 + 4097])
 def test_fp32_ragged_bands_and_segments(nq):
     """The FP32 sweep's 16-row lanes and 512-row bands against the oracle on
