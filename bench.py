@@ -311,7 +311,15 @@ def run_gpu(args):
     kms = statistics.median(kernel_ms)
     hms = statistics.median(heads_ms)
     achieved = FLOPS_PER_CELL * cells_per_step() / (kms * 1e-3)
-    traffic = args.traffic if args.traffic is not None else committed_traffic()
+    if args.traffic is not None:
+        traffic, traffic_src = args.traffic, "--traffic argument"
+    else:
+        traffic, traffic_src = measure_traffic()
+        if traffic is None:
+            why = traffic_src
+            traffic = committed_traffic()
+            traffic_src = ("committed ncu capture (profiles/r1_k_join_traffic.json); in-run measurement: " + why
+                           if traffic is not None else why)
     roofline = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": traffic,
                 "peak_measured": peak_meas / 1e12, "frac_of_measured": achieved / peak_meas,
@@ -319,8 +327,9 @@ def run_gpu(args):
                 "kernel": "k_join<8,false,false> (FP64 row-band join)", "achieved_def":
                     "6 FP64 flops per valid cell (profiles.hpp:330-331) x cells per launch / median duration of "
                     "the join kernel (CUDA events around its launch, on the launching stream)",
-                "traffic_def": "dram__bytes_read.sum + dram__bytes_write.sum of one k_join launch, ncu --set full "
-                               "capture of this bench command (profiles/r1_k_join_traffic.json)",
+                "traffic_def": "dram__bytes_read.sum + dram__bytes_write.sum of one k_join launch",
+                "traffic_source": traffic_src,
+                "algorithmic_bytes": algo_bytes_per_launch(),
                 "pipeline": {"join_ms_median": jms, "kernel_ms_median": kms, "heads_fft_ms_median": hms,
                              "frac": FLOPS_PER_CELL * cells_per_step() / (jms * 1e-3) / peak,
                              "def": "the whole join phase (column packing, FFT heads, join kernel, group merge)"},
@@ -655,6 +664,73 @@ def config_lines(args, dev, stream, flush, peak, nominal):
     return out
 
 
+def traffic_probe():
+    """--traffic-probe (internal): one C4 FP64 join on device-resident inputs,
+    the command measure_traffic() runs under ncu."""
+    import torch
+    import paper_2112_12965_b200 as tsd
+    D, _ = make_dictionary()
+    q = make_query(Q_SEED)
+    nrows = Q_LEN - M + 1
+    plan = tsd.DictPlan(D, M)
+    d_q = torch.from_numpy(q).cuda()
+    d_val = torch.empty(nrows, dtype=torch.float64, device="cuda")
+    d_idx = torch.empty(nrows, dtype=torch.int64, device="cuda")
+    plan.join_device(d_q.data_ptr(), [Q_LEN], d_val.data_ptr(), d_idx.data_ptr())
+    torch.cuda.synchronize()
+    plan.close()
+    return 0
+
+
+def measure_traffic(timeout_s=240):
+    """DRAM bytes of one C4 join-kernel launch, measured in this bench run:
+    ncu (dram__bytes_read.sum + dram__bytes_write.sum, the join kernel only)
+    over a one-join probe of the same workload in a child process (no bench
+    number is taken under the profiler). Returns (bytes, source) or (None,
+    why) when ncu is unavailable or fails; TSD_BENCH_NCU=0 skips it."""
+    import shutil
+    import subprocess
+    if os.environ.get("TSD_BENCH_NCU", "1") == "0":
+        return None, "skipped (TSD_BENCH_NCU=0)"
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if not ncu:
+        return None, "ncu not found"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "-k", "regex:k_join", "-c", "1", "--csv",
+           sys.executable, os.path.abspath(__file__), "--traffic-probe"]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout_s)
+    except (OSError, subprocess.TimeoutExpired) as e:
+        return None, "ncu failed: %s" % type(e).__name__
+    import csv
+    import io
+    vals = {}
+    lines = [l for l in r.stdout.splitlines() if l.startswith('"')]
+    for row in csv.DictReader(io.StringIO("\n".join(lines))):
+        name, unit = row.get("Metric Name"), row.get("Metric Unit", "")
+        try:
+            v = float(row.get("Metric Value", "").replace(",", ""))
+        except ValueError:
+            continue
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit)
+        if name and name.startswith("dram__bytes") and scale:
+            vals[name] = v * scale
+    if len(vals) != 2:
+        return None, "ncu returned no DRAM metrics (rc %d): %s" % (r.returncode, (r.stderr or r.stdout)[-200:])
+    return sum(vals.values()), ("measured in this run: " + " ".join(cmd[:-3]).replace(sys.executable, "python")
+                                + " bench.py --traffic-probe (one C4 join kernel launch)")
+
+
+def algo_bytes_per_launch():
+    """algorithmic bytes of one C4 join launch (SURVEY 8(d)'s
+    per-unit figures): the query's row data read once (df, dg, invn, mu: 32 B
+    per window), the dictionary's column data (32 B per column slot), and the
+    per-group results written (16 B per row and segment group is the
+    implementation's; the algorithm's output is 16 B per row)."""
+    nrows = Q_LEN - M + 1
+    return 32 * nrows + 32 * N_SEG * (SEG_LEN - M + 1) + 16 * nrows
+
+
 def committed_traffic():
     """DRAM bytes per k_join launch from the committed ncu capture of this workload, or None."""
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_k_join_traffic.json")
@@ -679,7 +755,10 @@ def main():
     ap.add_argument("--skip-configs", action="store_true", help="only the C4 headline (+ fp32, self-join) lines")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per join launch from an ncu capture (reported as roofline.traffic)")
+    ap.add_argument("--traffic-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.traffic_probe:
+        return traffic_probe()
     if args.warmup < 3:
         args.warmup = 3
     return run_reference(args) if args.impl == "reference" else run_gpu(args)

@@ -833,7 +833,8 @@ struct PipeState {
 };
 
 #ifndef TSD_LANE_THR64
-#define TSD_LANE_THR64 1
+#define TSD_LANE_THR64 0  // off: C4 539 -> 527 ms with it, but C5 +15 % and C3 +6 % (near-periodic data
+                          // passes the lane threshold on most steps); a per-segment adaptive switch cost more
 #endif
 // first level of the FP64 row test (TSD_LANE_THR64): the largest high word of
 // the lane's 8 values against the smallest slot threshold (VIMNMX3 tree);
