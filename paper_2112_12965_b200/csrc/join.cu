@@ -1567,7 +1567,7 @@ __device__ __forceinline__ void join_body(const JoinArgs& a) {
           S.mbk = min_bk16(S.BK);
           S.dirty = false;
           if constexpr (R == R32) sweep_segment32<SELF>(sm, cx, lane, FA, GA, S);
-        } else if (TSD_PIPE && !SYM) {
+        } else if constexpr (TSD_PIPE && !SYM) {
           PipeState<R> S;
           S.dirty = false;
           double dfa[R], dga[R];
@@ -2092,7 +2092,8 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     // the symmetric sweep takes 128 pieces (more, shorter tasks: self-joins
     // of 2^20-2^21 windows 0.5-3 % faster, 2^22 unchanged), AB joins 64
     const int64_t np64 = pn ? std::max<int64_t>(1, atoll(pn)) : (SYM ? 128 : 64);
-    const int64_t lmax = std::max<int64_t>(pe ? atoll(pe) : 2048, (tot + np64 - 1) / np64);
+    const int64_t lmax =
+        std::max<int64_t>(pe ? atoll(pe) : (in.min_tasks > 0 ? 256 : 2048), (tot + np64 - 1) / np64);
     for (const auto& s : in.segs) {
       const int64_t np = (s.ncol + lmax - 1) / lmax;
       if (np <= 1) {
@@ -2191,6 +2192,14 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
         if (nt <= nwarps) break;  // larger b only adds work per task
       }
     }
+  }
+  if (!SYM && in.min_tasks > 0) {
+    // small latency-bound joins (the self-join's coarse seed search): the
+    // most groups and the fewest bands per task that reach min_tasks tasks
+    // -- every warp of the GPU busy beats the cost model's merge savings
+    G = 1;
+    bpt = 1;
+    while (2 * G <= std::min(nseg, 64) && (int64_t)nbands * G < in.min_tasks) G *= 2;
   }
   if (!SYM && getenv("TSD_FORCE_G") && getenv("TSD_FORCE_BPT")) {  // development override
     G = std::max(1, std::min(nseg, atoi(getenv("TSD_FORCE_G"))));
@@ -2726,6 +2735,12 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     cin.m = md;
     cin.excl = (in.excl + f - 1) / f;
     cin.precision = 0;
+    {
+      // the coarse join is small (C2: 8.7k windows): plan it wide enough to
+      // occupy the GPU (C2 symmetric path: coarse join 0.83 -> ~0.3 ms)
+      const char* mt = getenv("TSD_COARSE_TASKS");  // development override
+      cin.min_tasks = mt ? atoi(mt) : 2400;
+    }
     const int64_t ncoarse = nd - md + 1;
     double* d_cbc = (double*)arena.get(sizeof(double) * ncoarse);
     int64_t* d_cbj = (int64_t*)arena.get(sizeof(int64_t) * ncoarse);

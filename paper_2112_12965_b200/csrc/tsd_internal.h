@@ -127,6 +127,8 @@ struct JoinInputs {
   double seed_margin = 0.0;
   // FP32 sweep: power-of-two scalings of the query / dictionary statistics (run_join)
   double f32_siga = 1.0, f32_sigb = 1.0;
+  // > 0: plan at least this many tasks (most groups, one band per task)
+  int min_tasks = 0;
 };
 
 // Runs the row-band join of every row against every valid column of every
