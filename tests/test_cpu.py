@@ -233,3 +233,22 @@ def test_sharded_self_join_exchange_two_ranks_gloo():
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "SELFSHARD_OK" in r.stdout
+
+
+def test_file_formats_match_reference(tmp_path):
+    """include/tsdict/io.hpp: the reference-written files of
+    tests/golden/io parse to the fixed objects, every golden document
+    (valid and corrupted) gets the reference parser's outcome, our files
+    round-trip (tests/cpp/test_io.cpp); and when the reference I/O driver was
+    built here (oracle/_ref/ref_io, unmodified reference io.hpp), it reads our
+    files back to the same objects."""
+    exe = os.path.join(ROOT, "tests", "cpp", "build", "test_io")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    r = subprocess.run([exe, str(tmp_path), os.path.join(ROOT, "tests", "golden", "io")], capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    ref = os.path.join(ROOT, "oracle", "_ref", "ref_io")
+    if os.path.exists(ref):
+        r = subprocess.run([ref, "read", str(tmp_path)], capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
