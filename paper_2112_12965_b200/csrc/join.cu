@@ -2582,6 +2582,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     k_merge_sym<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(d_pc, d_pj, nrows, G, d_ccand, in.cols.nwin,
                                                                   d_best_c, d_best_j);
     ++nl;
+    vmark("merge");
   } else if (G > 1) {
     k_merge_groups<<<(unsigned)((nrows + 255) / 256), 256, 0, st>>>(d_pc, d_pj, nrows, G);
     ++nl;
