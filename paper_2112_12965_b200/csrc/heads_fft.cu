@@ -237,6 +237,8 @@ struct HeadsArgs {
   double* heads;
   unsigned long long* seed;  // per row: order-preserving key of max_s head * kf (0 = none), or null
   int ppc;                   // pairs per CTA
+  int64_t tri_rows;          // > 0: skip column blocks below each segment's first read column (see tsd_internal.h)
+  long long tri_excl;
 };
 
 // A head (row i, column c) may seed row i only if row i's own sweep evaluates
@@ -275,7 +277,13 @@ __global__ void __launch_bounds__(FFT_T, 1) k_heads_fft(const HeadsArgs a) {
   double* dmu = reinterpret_cast<double*>(stw + FFT_N / 2);
   const int j = threadIdx.x;
   const int64_t blk0 = (int64_t)blockIdx.x * a.Q;
-  const int p0 = blockIdx.y * a.ppc, p1 = min(a.npairs, p0 + a.ppc);
+  const int p0 = blockIdx.y * a.ppc;
+  int p1 = min(a.npairs, p0 + a.ppc);
+  if (a.tri_rows > 0) {
+    // pairs whose first read column lies past this block (first columns grow with s)
+    while (p1 > p0 && ((((int64_t)(2 * (p1 - 1)) * a.tri_rows + a.tri_excl + 1) & ~int64_t(31)) >= blk0 + a.Q)) --p1;
+    if (p1 == p0) return;
+  }
   auto fetch = [&](int p) {
     const double2* sp = a.spec + (int64_t)p * FFT_N;
 #pragma unroll
@@ -353,7 +361,7 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
                       const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double* d_invn_b,
                       const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
                       unsigned long long* d_seed, long long excl, int sym, Arena& arena, cudaStream_t st,
-                      int* launches, Error* err) {
+                      int* launches, Error* err, int64_t tri_rows, long long tri_excl) {
   const int npairs = (nseg + 1) / 2;
   double2* d_tw = (double2*)arena.get(sizeof(double2) * FFT_N);
   double2* d_spec = (double2*)arena.get(sizeof(double2) * FFT_N * (size_t)npairs);
@@ -388,6 +396,8 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
   a.seed = d_seed;
   a.excl = excl;
   a.sym = sym;
+  a.tri_rows = tri_rows;
+  a.tri_excl = tri_excl;
   const int64_t nblk = (hrows + a.Q - 1) / a.Q;
   {
     // up to 64 pairs per CTA (one forward transform per 64 inverse ones),

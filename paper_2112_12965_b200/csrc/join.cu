@@ -2448,7 +2448,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
         ++nl;
         const int rc = compute_heads_fft(in.xb, in.nb, in.cols.nwin, in.cols.nwin, in.cols.mu, in.cols.flag, d_tw,
                                          d_tew, in.cols.invn, d_segs, nbr_t, m, d_te, tstride, nullptr, -1, 0, arena,
-                                         st, &nl, err);
+                                         st, &nl, err, SYM ? (int64_t)bpt * H : 0, SYM ? (long long)in.excl : 0);
         if (rc != kOk) return rc;
       } else {
         d_te = nullptr;

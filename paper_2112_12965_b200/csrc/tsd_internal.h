@@ -149,7 +149,11 @@ int compute_heads_fft(const double* d_x, int64_t na, int64_t nrows, int64_t hrow
                       const uint8_t* d_flag_a, const double* d_btil, const double* d_ebt, const double* d_invn_b,
                       const SegDev* d_segs, int nseg, int m, double* d_heads, int64_t hstride,
                       unsigned long long* d_seed, long long excl, int sym, Arena& arena, cudaStream_t st,
-                      int* launches, Error* err);
+                      int* launches, Error* err, int64_t tri_rows = 0, long long tri_excl = 0);
+// tri_rows > 0 (the symmetric self-join's FFT top edges): "segment" s is the
+// top window of rows [s * tri_rows, ...), whose sweep reads only the columns
+// from ((s * tri_rows + tri_excl + 1) & ~31) on; column blocks entirely below
+// that are skipped (about half the table).
 
 // learn.cu -------------------------------------------------------------------
 // Device steps of the greedy learning loop (dictionary.hpp:279-316): argmin of
