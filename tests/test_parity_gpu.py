@@ -513,6 +513,28 @@ def test_fp32_scaling_and_fp64_fallback(capfd, monkeypatch):
     assert st["max_abs"] <= 1e-3
 
 
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_near_periodic_batched_join(precision):
+    """C5-style near-periodic data (daily / weekly sinusoids, noise, level
+    shifts): most steps pass the block threshold and rows' bests rise often,
+    so the exact paths (FP64 may-check and shared update; FP32 lane test,
+    per-slot test and shared update) run constantly. Batched join of 6
+    series against a 16-segment dictionary, all rows against the oracle."""
+    m = 128
+    series = synth.traffic(6, 6, 4096)
+    src = synth.traffic(7, 1, 40000)[0]
+    segs = [src[2048 * k: 2048 * k + 1024].copy() for k in range(16)]
+    starts = [2048 * k for k in range(16)]
+    D = _dict(segs, starts, m)
+    Ps = tsd.join_dictionary_batched(list(series), D, m, precision=precision)
+    for k, (s, P) in enumerate(zip(series, Ps)):
+        rv, ri = O.dict_join(s, segs, starts, m)
+        st = check_profile(P.values, P.indices, rv, ri, m, dict_dist(s, segs, starts, m), fp32=precision == "fp32",
+                           label=f"periodic batched {precision} series {k}")
+        if precision == "fp32":
+            assert st["max_abs"] <= 1e-3
+
+
 @pytest.mark.parametrize("order", ["quiet_then_huge", "huge_then_quiet"])
 def test_window_stats_and_join_across_huge_excursions(order):
     """Window statistics over one buffer holding 1e-6-scale and 1e60-scale
