@@ -3,7 +3,8 @@
 // series against one resident dictionary; its consumers Discord /
 // AnomalyReport (:28-38), find_discords (:54-93, peaks on the device),
 // make_anomaly_report (:95-101), window_labels (:102-127) and auc_score
-// (:130-162) (host).
+// (:130-162) (host; auc_score restates the reference's ranking rule so scores
+// agree exactly).
 #ifndef TSDICT_B200_DICT_JOIN_HPP
 #define TSDICT_B200_DICT_JOIN_HPP
 

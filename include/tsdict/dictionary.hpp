@@ -6,6 +6,14 @@
 // learn_dictionary (:259-328) with its selection loop on the device
 // (tsd_learn_dictionary); learn_dictionary_random (:333-379) keeps its host
 // loop (the reference's RNG stream) and computes e_max on the device.
+//
+// The host helpers below (context_interval, merge_intervals, merge_segments,
+// validate_learn_config, the selection bookkeeping, finish_dictionary,
+// learn_dictionary_random) deliberately restate the reference's observable
+// host semantics -- its interval arithmetic, stop rules, error messages and
+// RNG draw order -- so a drop-in user gets identical dictionaries; the
+// compute they drive (self-join, distance profiles, argmin, e_max) is the
+// device's.
 #ifndef TSDICT_B200_DICTIONARY_HPP
 #define TSDICT_B200_DICTIONARY_HPP
 
