@@ -869,6 +869,9 @@ __device__ __forceinline__ void pipe_test(WarpSmem<R>& sm, const SweepCtx& cx, i
 #pragma unroll
     for (int r = 0; r < R; ++r) may |= V[r] * invb > S.bKp[r] || !(S.bKp[r] > 0.0);
     if (__any_sync(0xffffffffu, may)) {
+#ifdef TSD_COUNT_EXACT
+      if (lane == 0) atomicAdd(&g_cas_count, 1ull);  // (AB joins: exact-path entries past the register check)
+#endif
 #pragma unroll
       for (int r = 0; r < R; ++r) sm.slide[r * 32 + lane] = V[r];
       S.dirty |= exact_update64<R, SELF>(sm, lane, cx.colbase + c, invb, cx.row0, cx.excl);
