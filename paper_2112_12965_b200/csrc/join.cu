@@ -2441,8 +2441,12 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     tstride = (in.cols.nwin + 1) & ~int64_t(1);
     size_t fr = 0;
     const size_t tbytes = sizeof(double) * (size_t)nbr_t * (size_t)tstride;
-    if ((e ? atoi(e) != 0 : true) && heads_fft_supported(m) && nbr_t >= 2 &&
-        device_free_bytes(&fr) && tbytes < fr / 4) {
+    // small joins compute their top edges in the kernel: below ~2^30 FMAs of
+    // direct dot products the FFT pre-pass's four launches cost more (C1:
+    // 0.343 -> 0.320 ms per step)
+    const bool big = (double)nbr_t * (double)total_cols * (double)m > 1073741824.0;
+    if ((e ? atoi(e) != 0 : big) && heads_fft_supported(m) && nbr_t >= 2 && device_free_bytes(&fr) &&
+        tbytes < fr / 4) {
       double* d_tw = (double*)arena.get(sizeof(double) * (size_t)nbr_t * m);
       double* d_tew = (double*)arena.get(sizeof(double) * nbr_t);
       d_te = (double*)arena.get(tbytes);
