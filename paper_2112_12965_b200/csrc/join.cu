@@ -2165,7 +2165,12 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   {
     double best = 1e300;
     std::vector<int> gs;
-    for (int g = 1; g <= nseg && g <= 64; g *= 2) {
+    // round-2 re-calibration for AB / dictionary joins (measured on C4, C3,
+    // C5): at most 16 segment groups, plans up to 32 waves, and the FFT
+    // top-edge pre-pass costed; the self-join's full-matrix sweep keeps the
+    // round-1 model (64 pieces, 16 waves: C2 5.0 vs 5.5-5.8 ms otherwise)
+    const int gmax = SELF ? 64 : 16, wave_cap = SELF ? 16 : 32;
+    for (int g = 1; g <= nseg && g <= gmax; g *= 2) {
       split(g, gs);
       int64_t cmax = 0, smax = 0;
       for (int q = 0; q < g; ++q) {
@@ -2183,10 +2188,16 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       const int bmax = std::min(nbands, F32 ? 4096 / H : 4096);
       for (int b = 1; b <= bmax; ++b) {
         const int64_t nt = (int64_t)((nbands + b - 1) / b) * g;
-        if (nt > 16 * (int64_t)nwarps) continue;
+        if (nt > (int64_t)wave_cap * nwarps) continue;
         const double tc = b * band + top;
         const double run = nt <= nwarps ? 1.25 * tc * nwarps / (double)nt : (double)nt * tc / nwarps + 0.5 * tc;
-        const double cost = run + (g > 1 ? 30.0 * (double)nrows * g / nwarps : 0.0);
+        // the FFT top-edge pre-pass, one table row per band range over all
+        // columns, in the same per-warp units (C4: 3.2 ms for 2341 x 131328).
+        // With it and 32 waves C4 takes 14 bands per task instead of 28
+        // (kernel 537 -> 525 ms, step 565 -> 557 ms)
+        const double pre =
+            !SELF && fft && nseg >= 2 ? 0.058 * (double)((nbands + b - 1) / b) * (double)total_cols : 0.0;
+        const double cost = run + pre + (g > 1 ? 30.0 * (double)nrows * g / nwarps : 0.0);
         if (cost < best * 0.999) {
           best = cost;
           G = g;
