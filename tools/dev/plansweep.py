@@ -1,3 +1,5 @@
+"""Forced decomposition plans on C4 (development tool): kernel and step ms
+for G in 4..32 and several bands per task. usage: python tools/dev/plansweep.py fp32|fp64"""
 import sys, os
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
