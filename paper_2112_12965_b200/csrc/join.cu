@@ -2270,11 +2270,16 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     const int bpmax = std::min(nbands, 1024);
     const char* bpe = getenv("TSD_SYM_BP");  // development override of the bands per task
     const int bpforce = bpe ? atoi(bpe) : 0;
-    for (int bp = 1; bp <= bpmax; bp *= 2) {
-      if (bpforce > 0 && bp != bpforce) continue;
+    std::vector<int> bps;
+    if (bpforce > 0) {
+      bps.push_back(std::min(bpforce, nbands));
+    } else {
+      for (int bp = 1; bp <= bpmax; bp *= 2) bps.push_back(bp);
+    }
+    for (const int bp : bps) {
       // very fine splits only add per-task overhead (top edge, head) once
       // there are many tasks per warp; skip them while a coarser one remains
-      if (bp * 2 <= bpmax) {
+      if (bp * 2 <= bpmax && bpforce <= 0) {
         int64_t cnt = 0;
         for (int g = 0; g < G; ++g)
           for (int b0 = 0; b0 < nbands; b0 += bp) cnt += qoff(b0, g) < segs[g].ncol;
@@ -2330,6 +2335,12 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
       break;
     }
     bpt = bbest;
+    // every band range with cells yields a task, so a plan without tasks can
+    // only be a planning fault (its epilogue would report every row empty)
+    if (plans.empty() || (sym_tasks.empty() && in.nshards <= 1)) {
+      if (err) *err = Error{kCudaError, "internal: the symmetric self-join plan has no tasks"};
+      return kCudaError;
+    }
     sym_cache.key = sym_key;
     sym_cache.tasks = sym_tasks;
     sym_cache.bpt = bpt;
