@@ -79,6 +79,9 @@ constexpr int T = 64;     // head / top-edge staging chunk (samples)
 #ifndef TSD_NREG_SYM
 #define TSD_NREG_SYM 0  // symmetric self-join sweep
 #endif
+#ifndef TSD_PRED_EDGE
+#define TSD_PRED_EDGE 1  // lane 0's incoming diagonal by a predicated load over its shuffle result (no select)
+#endif
 #ifndef TSD_PIPE
 #define TSD_PIPE 1  // the software-pipelined FP64 sweep (sweep_segment_p) for the AB / full-matrix joins
 #endif
@@ -197,10 +200,30 @@ __device__ __forceinline__ double shfl_up1(double v) {
 
 // warp vote over R = 8 slot tests "hi(c~) >= thr": two independent 4-deep
 // predicate chains joined by one OR (ptxas otherwise builds one 8-deep chain)
-template <int R>
+#ifndef TSD_VOTE1
+#define TSD_VOTE1 1  // pipelined AB sweep: C4-shape kernel -1 %; the symmetric sweep keeps two chains (+5 % with one)
+#endif
+template <int R, bool CHAIN1 = false>
 __device__ __forceinline__ bool vote_any8(const double (&P)[R], int ph, const int (&thr)[R]) {
   static_assert(R == 8, "vote_any8 is written for R = 8");
   unsigned r;
+  if (CHAIN1) {  // one 8-deep predicate chain (no PLOP3 join): the pipelined sweep tests a column while
+                 // the next one's DFMAs issue, so the longer chain stays off its critical path
+    asm volatile(
+        "{\n .reg .pred a;\n"
+        " setp.ge.s32 a, %1, %9;\n setp.ge.or.s32 a, %2, %10, a;\n"
+        " setp.ge.or.s32 a, %3, %11, a;\n setp.ge.or.s32 a, %4, %12, a;\n"
+        " setp.ge.or.s32 a, %5, %13, a;\n setp.ge.or.s32 a, %6, %14, a;\n"
+        " setp.ge.or.s32 a, %7, %15, a;\n setp.ge.or.s32 a, %8, %16, a;\n"
+        " vote.sync.any.pred a, a, -1;\n selp.u32 %0, 1, 0, a;\n}\n"
+        : "=r"(r)
+        : "r"(__double2hiint(P[(0 + ph) & 7])), "r"(__double2hiint(P[(1 + ph) & 7])),
+          "r"(__double2hiint(P[(2 + ph) & 7])), "r"(__double2hiint(P[(3 + ph) & 7])),
+          "r"(__double2hiint(P[(4 + ph) & 7])), "r"(__double2hiint(P[(5 + ph) & 7])),
+          "r"(__double2hiint(P[(6 + ph) & 7])), "r"(__double2hiint(P[(7 + ph) & 7])), "r"(thr[0]), "r"(thr[1]),
+          "r"(thr[2]), "r"(thr[3]), "r"(thr[4]), "r"(thr[5]), "r"(thr[6]), "r"(thr[7]));
+    return r != 0;
+  }
   asm volatile(
       "{\n .reg .pred a, b;\n"
       " setp.ge.s32 a, %1, %9;\n setp.ge.s32 b, %5, %13;\n"
@@ -567,7 +590,7 @@ struct StepIn {
   double dfb, dgb, e, in, nmin;  // nmin: loaded with the first column of a threshold block
 };
 
-__device__ __forceinline__ void prefetch(bool nm, const double4* cb, const double* ep, double v7, StepIn& d) {
+__device__ __forceinline__ void prefetch(bool nm, const double4* cb, const double* ep, double v7, StepIn& d, bool l0) {
   if (nm) {  // constant after unrolling
     const double4 c = *cb;
     d.dfb = c.x;
@@ -578,8 +601,11 @@ __device__ __forceinline__ void prefetch(bool nm, const double4* cb, const doubl
     d.dfb = c.x;
     d.dgb = c.y;
   }
-  d.e = *ep;
   d.in = shfl_up1(v7);
+  // lane 0 overwrites its shuffle result with the band above's edge (a
+  // predicated load instead of a per-step select on the ALU pipe)
+  if (TSD_PRED_EDGE && l0) d.in = *ep;
+  if (!TSD_PRED_EDGE) d.e = *ep;
 }
 
 template <int R>
@@ -679,7 +705,7 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
     if (!(FIRST && u == 0)) {
       // fold in the incoming diagonal; lane 31 retires its bottom-row value (column k-1)
       (u == 0 ? st_prev : st_cur + u - 1)[0] = S.P[ph];
-      S.P[ph] = l0 ? S.nx.e : S.nx.in;
+      S.P[ph] = TSD_PRED_EDGE ? S.nx.in : l0 ? S.nx.e : S.nx.in;
       const double dfb = S.nx.dfb, dgb = S.nx.dgb;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -689,7 +715,7 @@ __device__ __forceinline__ void sweep_block(WarpSmem<R>& sm, const SweepCtx& cx,
     }
     if (!GUARD || k + 1 < n)
       prefetch((u + 1) % TB == 0, u + 1 < R ? ccur + u + 1 : cnext, &sm.ering[ebase + u],
-               S.P[(ph + R - 1) & (R - 1)], S.nx);
+               S.P[(ph + R - 1) & (R - 1)], S.nx, l0);
 #ifdef TSD_ABL_NOEXACT
     unsigned opaque0;  // 0, invisible to the compiler: the test stays, the exact update never runs
     asm volatile("mov.u32 %0, 0;" : "=r"(opaque0));
@@ -860,7 +886,7 @@ __device__ __forceinline__ void pipe_test(WarpSmem<R>& sm, const SweepCtx& cx, i
   // the lane threshold too often -- C2 5.07 -> 5.15 ms with it, C4 539 -> 527 ms)
   if (TSD_LANE_THR64 && !SELF && !vote_lane8(V, S.lthr)) [[likely]]
     return;
-  if (vote_any8(V, 0, S.thr)) [[unlikely]] {
+  if (vote_any8<R, TSD_VOTE1 != 0>(V, 0, S.thr)) [[unlikely]] {
 #ifdef TSD_COUNT_EXACT
     if (lane == 0) atomicAdd(&g_exact_count, 1ull);
 #endif
@@ -907,7 +933,7 @@ __device__ __forceinline__ void sweep_block_p(WarpSmem<R>& sm, const SweepCtx& c
       // column k from column k - 1: slots 7..1 first (slot 7 feeds the next shuffle)
 #pragma unroll
       for (int r = R - 1; r >= 1; --r) D[r] = __fma_rn(dga[r], S.dfb, __fma_rn(dfa[r], S.dgb, V[r - 1]));
-      const double x0 = l0 ? S.e : S.in;
+      const double x0 = TSD_PRED_EDGE ? S.in : l0 ? S.e : S.in;
       D[0] = __fma_rn(dga[0], S.dfb, __fma_rn(dfa[0], S.dgb, x0));
       // lane 31 retires its bottom row of column k - 1 into the edge ring
       (u == 0 ? st_prev : st_cur + u - 1)[0] = V[R - 1];
@@ -925,9 +951,12 @@ __device__ __forceinline__ void sweep_block_p(WarpSmem<R>& sm, const SweepCtx& c
         S.dfb = c2.x;
         S.dgb = c2.y;
       }
-      S.e = sm.ering[m96 + u];
+      if (!TSD_PRED_EDGE) S.e = sm.ering[m96 + u];
     }
     S.in = shfl_up1(D[R - 1]);
+    // TSD_PRED_EDGE: lane 0 overwrites its (unused) shuffle result with the
+    // band above's edge by a predicated load -- no per-step select on the ALU pipe
+    if (TSD_PRED_EDGE && l0) S.in = sm.ering[m96 + u];
     if (!(FIRST && u == 0)) {
       // test column k - 1 with the thresholds of its block
       pipe_test<R, SELF>(sm, cx, lane, S, V, k - 1, u == 0 ? (m96 == 0 ? 95 : m96 - 1) : m96 + u - 1);
@@ -1073,12 +1102,13 @@ struct StepIn32 {
   float e, in;
 };
 
-__device__ __forceinline__ void prefetch32(const Col32* cb, const float* ep, float v15, StepIn32& d) {
+__device__ __forceinline__ void prefetch32(const Col32* cb, const float* ep, float v15, StepIn32& d, bool l0) {
   const ulonglong2 a = *reinterpret_cast<const ulonglong2*>(cb);
   d.dg2 = a.x;
   d.df2 = a.y;
-  d.e = *ep;
   d.in = shfl_up1f(v15);
+  if (TSD_PRED_EDGE && l0) d.in = *ep;  // as prefetch(): no per-step select
+  if (!TSD_PRED_EDGE) d.e = *ep;
 }
 
 constexpr int R32 = 16;  // rows per lane in the FP32 sweep
@@ -1233,14 +1263,14 @@ __device__ __forceinline__ void sweep_block32(WarpSmem<R32>& sm, const SweepCtx&
       // slot 15 (bottom row, column k-1); slot 8 takes the lane's own slot 7
       const u64 old = S.Q[ph];
       (u == 0 ? st_prev : st_cur + u - 1)[0] = hi2(old);
-      S.Q[ph] = pack2(l0 ? S.nx.e : S.nx.in, lo2(old));
+      S.Q[ph] = pack2(TSD_PRED_EDGE ? S.nx.in : l0 ? S.nx.e : S.nx.in, lo2(old));
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int a = (q - ph + 8) & 7;
         S.Q[q] = fma2(GA[a], S.nx.df2, fma2(FA[a], S.nx.dg2, S.Q[q]));  // profiles.hpp:330
       }
     }
-    if (!GUARD || k + 1 < n) prefetch32(u + 1 < 8 ? ccur + u + 1 : cnext, &ring[ebase + u], hi2(S.Q[(ph + 7) & 7]), S.nx);
+    if (!GUARD || k + 1 < n) prefetch32(u + 1 < 8 ? ccur + u + 1 : cnext, &ring[ebase + u], hi2(S.Q[(ph + 7) & 7]), S.nx, l0);
     // two-level test: the lane threshold (VIMNMX3 trees) first, the 16 slot
     // thresholds only when some lane passes it
     bool pass = TSD_LANE_THR32 ? vote_lane16f(S.Q, lthr) : true;
@@ -1286,7 +1316,7 @@ __device__ void sweep_segment32(WarpSmem<R32>& sm, const SweepCtx& cx, int lane,
   int flushed = 0;
   if (n > 1)
     prefetch32(reinterpret_cast<const Col32*>(&sm.colbuf[0][1]), reinterpret_cast<const float*>(sm.ering),
-               hi2(S.Q[7]), S.nx);
+               hi2(S.Q[7]), S.nx, l0);
   auto chunk_turn = [&](int c) {
     __syncwarp();
     if (c >= 2 && cx.write_out) {

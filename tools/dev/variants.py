@@ -17,7 +17,10 @@ for c in %r:
     f = c.split(":")
     if f[0] == "dict":
         nq, nseg, L, m = map(int, f[1:5]); prec = f[5] if len(f) > 5 else "fp64"
-        q = synth.walk(4, nq); segs = synth.walks(5, nseg, L)
+        if os.environ.get("DICTKIND") == "traffic":  # C5-like near-periodic query and dictionary
+            q = synth.traffic(6, 1, nq)[0]; segs = synth.traffic(7, nseg, L)
+        else:
+            q = synth.walk(4, nq); segs = synth.walks(5, nseg, L)
         D = t.Dictionary([t.Segment(L * s, segs[s]) for s in range(nseg)], m=m, source_length=nseg * L)
         plan = t.DictPlan(D, m, prec)
         dq = torch.from_numpy(q).cuda(); cnt = nq - m + 1
