@@ -143,7 +143,8 @@ struct JoinArgs {
   int nwarps_alloc;              // warps with edge / head scratch
 };
 
-template <int R>
+// W: the wide FP64 sweep (R = 16 rows per lane with FP64 bests)
+template <int R, bool W = false>
 struct __align__(16) WarpSmem {
   double4 colbuf[3][32];
   double ering[96];
@@ -165,7 +166,7 @@ struct __align__(16) WarpSmem {
   // best K = cov * invn_b per slot (row factor invn_a left out); +inf =
   // inactive row. The FP32 sweep (R = 16) keeps FP32 bests: float storage
   // fits its 16 rows per lane in 8 CTAs per SM
-  std::conditional_t<R == 8, double, float> bK[R][32];
+  std::conditional_t<R == 8 || W, double, float> bK[R][32];
   int bj[R][32];     // its concatenated column
   double slide[Geo<R>::SLIDE];
   double unif[T];
@@ -243,8 +244,8 @@ __device__ __forceinline__ bool vote_any8(const double (&P)[R], int ph, const in
 
 // out[r] = sum_{t<m} U[t] * (S[R*lane + r + t] - cS), U[t] = Ug[t] - cu.
 // S samples at index >= s_avail read as cS (contribute 0). Returns sum U in *esum.
-template <int R>
-__device__ void sliding_dot(WarpSmem<R>& sm, const double* __restrict__ Ug, double cu, const double* __restrict__ Sg,
+template <int R, bool W>
+__device__ void sliding_dot(WarpSmem<R, W>& sm, const double* __restrict__ Ug, double cu, const double* __restrict__ Sg,
                             int64_t s_avail, double cS, int m, int lane, double (&out)[R], double* esum) {
   constexpr int H = Geo<R>::H;
 #pragma unroll
@@ -371,8 +372,8 @@ struct SweepCtx {
 
 // chunk c of the segment: column data for steps [32c, 32c+32) -> colbuf[c%3],
 // edge block c (E[32c .. 32c+31]) -> ring slot c%3
-template <int R>
-__device__ __forceinline__ void issue_chunk(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int c) {
+template <int R, bool W>
+__device__ __forceinline__ void issue_chunk(WarpSmem<R, W>& sm, const SweepCtx& cx, int lane, int c) {
   const double4* src = cx.colg + 32 * c + lane;
   double4* dst = &sm.colbuf[c % 3][lane];
   cp16(dst, src);
@@ -396,8 +397,8 @@ __device__ __forceinline__ void fold_cmin(WarpSmem<R>& sm, int lane, int c) {
   __syncwarp();
 }
 
-template <int R>
-__device__ __forceinline__ void flush_block(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int b) {
+template <int R, bool W>
+__device__ __forceinline__ void flush_block(WarpSmem<R, W>& sm, const SweepCtx& cx, int lane, int b) {
   const int j = 32 * b + lane;
   TSD_CHECK(b >= 0 && (b % 3) * 32 + lane < 96);
   if (j < cx.ncol - 1) cx.E[j] = sm.ering[(b % 3) * 32 + lane];
@@ -624,8 +625,8 @@ struct SweepState {
 // increasing order, so ties keep the lower column, profiles.hpp:70-77; a flat
 // column has invn_b = 0 -> K = 0, :332-336). Returns whether any best of the
 // warp changed.
-template <int R, bool SELF>
-__device__ __noinline__ bool exact_update64(WarpSmem<R>& sm, int lane, int col, double invb, long long row0,
+template <int R, bool SELF, bool W>
+__device__ __noinline__ bool exact_update64(WarpSmem<R, W>& sm, int lane, int col, double invb, long long row0,
                                             long long excl) {
   bool any = false;
 #ifdef TSD_COUNT_EXACT
@@ -1037,6 +1038,181 @@ __device__ void sweep_segment_p(WarpSmem<R>& sm, const SweepCtx& cx, int lane, c
 }
 
 // ===========================================================================
+// Wide FP64 sweep (AB / dictionary joins, TSD_WIDE=1): 16 rows per lane, bands
+// of 512 rows. A step's fixed costs -- the shuffle, the column and edge loads,
+// the bottom-row store, the vote and the branch over the exact path -- are
+// shared by 32 DFMAs instead of 16, and a warp carries 16 independent
+// two-DFMA chains, so fewer resident warps keep the FP64 pipe fed. The column
+// is updated IN PLACE from the highest slot down (slot r reads slot r - 1 of
+// the previous column before that register is overwritten), so one register
+// set holds the band and nothing rotates; the test of column k runs right
+// after its DFMAs. Cells, operations and their order are the R = 8 sweep's,
+// so profiles are bitwise identical.
+// ===========================================================================
+#ifndef TSD_JOIN_MINB_WIDE
+#define TSD_JOIN_MINB_WIDE 6
+#endif
+#ifndef TSD_WIDE_DEFAULT
+#define TSD_WIDE_DEFAULT 0
+#endif
+#ifndef TSD_WIDE_MIN_ROWS
+#define TSD_WIDE_MIN_ROWS (1 << 20)
+#endif
+constexpr int RW = 16;
+
+template <int R>
+struct WideState {
+  double P[R];    // slot r's covariance at the current column
+  double bKp[R];  // kplus(bestK)
+  int thr[R];     // hi(bKp * nmin) of the current threshold block
+  double dfb, dgb, in, nmin;  // prefetched column data / incoming diagonal of the next column
+  bool dirty;
+};
+
+// warp vote over 16 slot tests "hi(cov) >= thr" (four 4-deep predicate chains)
+__device__ __forceinline__ bool vote_any16d(const double (&P)[16], const int (&t)[16]) {
+  int h[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) h[r] = __double2hiint(P[r]);
+  unsigned r;
+  asm volatile(
+      "{\n .reg .pred a, b, c, d;\n"
+      " setp.ge.s32 a, %1, %17;\n setp.ge.s32 b, %5, %21;\n setp.ge.s32 c, %9, %25;\n setp.ge.s32 d, %13, %29;\n"
+      " setp.ge.or.s32 a, %2, %18, a;\n setp.ge.or.s32 b, %6, %22, b;\n"
+      " setp.ge.or.s32 c, %10, %26, c;\n setp.ge.or.s32 d, %14, %30, d;\n"
+      " setp.ge.or.s32 a, %3, %19, a;\n setp.ge.or.s32 b, %7, %23, b;\n"
+      " setp.ge.or.s32 c, %11, %27, c;\n setp.ge.or.s32 d, %15, %31, d;\n"
+      " setp.ge.or.s32 a, %4, %20, a;\n setp.ge.or.s32 b, %8, %24, b;\n"
+      " setp.ge.or.s32 c, %12, %28, c;\n setp.ge.or.s32 d, %16, %32, d;\n"
+      " or.pred a, a, b;\n or.pred c, c, d;\n or.pred a, a, c;\n"
+      " vote.sync.any.pred a, a, -1;\n selp.u32 %0, 1, 0, a;\n}\n"
+      : "=r"(r)
+      : "r"(h[0]), "r"(h[1]), "r"(h[2]), "r"(h[3]), "r"(h[4]), "r"(h[5]), "r"(h[6]), "r"(h[7]), "r"(h[8]),
+        "r"(h[9]), "r"(h[10]), "r"(h[11]), "r"(h[12]), "r"(h[13]), "r"(h[14]), "r"(h[15]), "r"(t[0]),
+        "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]), "r"(t[8]),
+        "r"(t[9]), "r"(t[10]), "r"(t[11]), "r"(t[12]), "r"(t[13]), "r"(t[14]), "r"(t[15]));
+  return r != 0;
+}
+
+// one block of TB steps from column k0 (k0 % TB == 0)
+template <int R, bool SELF, bool FIRST, bool GUARD>
+__device__ __forceinline__ void sweep_block_w(WarpSmem<R, true>& sm, const SweepCtx& cx, int lane, int k0, int m96,
+                                              WideState<R>& S, const double (&dfa)[R], const double (&dga)[R],
+                                              double* sbase, bool l0) {
+  static_assert(R == 16 && TB == 8, "the wide sweep is written for R = 16 with 8-column threshold blocks");
+  const int n = cx.ncol;
+  const double4* cflat = &sm.colbuf[0][0];
+  const double4* ccur = cflat + m96;
+  const double4* cnext = cflat + (m96 + TB == 96 ? 0 : m96 + TB);
+  double* const st_prev = sbase + (m96 == 0 ? 95 : m96 - 1);  // ring slot of column k0 - 1
+  double* const st_cur = sbase + m96;
+#pragma unroll
+  for (int u = 0; u < TB; ++u) {
+    const int k = k0 + u;
+    if (GUARD && k >= n) break;
+    if (u == 0) {  // column k opens a threshold block
+      if (FIRST) S.nmin = ccur[0].w;
+      if (S.dirty) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) S.bKp[r] = kplus(sm.bK[r][lane]);
+        S.dirty = false;
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) S.thr[r] = __double2hiint(S.bKp[r] * S.nmin);
+    }
+    if (!(FIRST && u == 0)) {
+      // lane 31 retires its bottom row of column k - 1 into the edge ring
+      (u == 0 ? st_prev : st_cur + u - 1)[0] = S.P[R - 1];
+      // column k in place, highest slot first (slot 15 feeds the next shuffle)
+#pragma unroll
+      for (int r = R - 1; r >= 1; --r) S.P[r] = __fma_rn(dga[r], S.dfb, __fma_rn(dfa[r], S.dgb, S.P[r - 1]));
+      S.P[0] = __fma_rn(dga[0], S.dfb, __fma_rn(dfa[0], S.dgb, S.in));  // profiles.hpp:330
+    }
+    // prefetch column k + 1: column data, the shuffled slot 15, lane 0's edge
+    if (!GUARD || k + 1 < n) {
+      const double4* cb = u + 1 < TB ? ccur + u + 1 : cnext;
+      if ((u + 1) % TB == 0) {
+        const double4 c4 = *cb;
+        S.dfb = c4.x;
+        S.dgb = c4.y;
+        S.nmin = c4.w;
+      } else {
+        const double2 c2 = *reinterpret_cast<const double2*>(cb);
+        S.dfb = c2.x;
+        S.dgb = c2.y;
+      }
+    }
+    S.in = shfl_up1(S.P[R - 1]);
+    if (l0) S.in = sm.ering[m96 + u];  // predicated load over the shuffle result (no select)
+    if (vote_any16d(S.P, S.thr)) [[unlikely]] {
+#ifdef TSD_COUNT_EXACT
+      if (lane == 0) atomicAdd(&g_exact_count, 1ull);
+#endif
+      const double invb = ccur[u].z;
+      bool may = false;
+#pragma unroll
+      for (int r = 0; r < R; ++r) may |= S.P[r] * invb > S.bKp[r] || !(S.bKp[r] > 0.0);
+      if (__any_sync(0xffffffffu, may)) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm.slide[r * 32 + lane] = S.P[r];
+        S.dirty |= exact_update64<R, SELF>(sm, lane, cx.colbase + k, invb, cx.row0, cx.excl);
+      }
+    }
+  }
+}
+
+template <int R, bool SELF>
+__device__ void sweep_segment_w(WarpSmem<R, true>& sm, const SweepCtx& cx, int lane, const double (&dfa)[R],
+                                const double (&dga)[R], WideState<R>& S) {
+  const int n = cx.ncol;
+  const int nchunks = (n + 31) >> 5;
+  // lanes 0..30 store their (unused) slot 15 into scratch past the staged slot values
+  double* const sbase = lane == 31 ? sm.ering : sm.slide + 32 * R;
+  const bool l0 = lane == 0;
+  __syncwarp();
+  issue_chunk(sm, cx, lane, 0);
+  if (nchunks > 1) issue_chunk(sm, cx, lane, 1); else cp_commit();
+  cp_wait<1>();
+  __syncwarp();
+  int flushed = 0;
+  auto chunk_turn = [&](int c) {
+    __syncwarp();
+    if (c >= 2 && cx.write_out) {
+      flush_block(sm, cx, lane, c - 2);
+      flushed = c - 1;
+    }
+    __syncwarp();
+    if (c + 1 < nchunks) issue_chunk(sm, cx, lane, c + 1); else cp_commit();
+    cp_wait<1>();
+    __syncwarp();
+  };
+  constexpr int BPC = 32 / TB;
+  if (n <= TB) {
+    sweep_block_w<R, SELF, true, true>(sm, cx, lane, 0, 0, S, dfa, dga, sbase, l0);
+  } else {
+    sweep_block_w<R, SELF, true, false>(sm, cx, lane, 0, 0, S, dfa, dga, sbase, l0);
+    int k0 = TB, m96 = TB, bic = 1;
+    for (; k0 + TB <= n; k0 += TB) {
+      if (bic == BPC - 1 && k0 + TB < n) chunk_turn((k0 + TB) >> 5);
+      sweep_block_w<R, SELF, false, false>(sm, cx, lane, k0, m96, S, dfa, dga, sbase, l0);
+      m96 = m96 + TB == 96 ? 0 : m96 + TB;
+      bic = bic == BPC - 1 ? 0 : bic + 1;
+    }
+    if (k0 < n) sweep_block_w<R, SELF, false, true>(sm, cx, lane, k0, m96, S, dfa, dga, sbase, l0);
+  }
+  cp_wait<0>();
+  __syncwarp();
+#ifdef TSD_COUNT_EXACT
+  if (lane == 0) atomicAdd(&g_step_count, (unsigned long long)n);
+#endif
+  if (cx.write_out) {
+    const int last = (n - 2) >> 5;
+    for (int b = flushed; b <= last && n >= 2; ++b) flush_block(sm, cx, lane, b);
+  }
+  __syncwarp();
+}
+
+// ===========================================================================
 // FP32 mode: the same sweep as FP64 in FP32 arithmetic -- the reference's
 // unnormalised centred recurrence cov = fma(dg_a, df_b, fma(df_a, dg_b, cov))
 // (profiles.hpp:330), two cells per fma.rn.f32x2 (FFMA2), 2 FP32 FMAs per
@@ -1184,7 +1360,6 @@ __device__ __forceinline__ bool vote_lane16f(const u64 (&Q)[8], int thr) {
 #ifndef TSD_LANE_THR32
 #define TSD_LANE_THR32 1
 #endif
-
 template <int R>
 __device__ __forceinline__ void issue_chunk32(WarpSmem<R>& sm, const SweepCtx& cx, int lane, int c) {
   const double4* src = cx.colg + 32 * c + lane;
@@ -1360,9 +1535,10 @@ __device__ __forceinline__ void join_body(const JoinArgs& a) {
   static_assert(!SYM || (SELF && !F32), "the symmetric sweep is the FP64 self-join");
   constexpr int H = Geo<R>::H;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  WarpSmem<R>* smem = reinterpret_cast<WarpSmem<R>*>(smem_raw);
+  using SM = WarpSmem<R, (R == 16 && !F32)>;
+  SM* smem = reinterpret_cast<SM*>(smem_raw);
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  WarpSmem<R>& sm = smem[wl];
+  SM& sm = smem[wl];
   const int gw = blockIdx.x * WARPS + wl;
   double* Ew = a.edges + (int64_t)gw * a.ecap;
   double* Hw = a.hscr + (int64_t)gw * 2048;
@@ -1600,6 +1776,21 @@ __device__ __forceinline__ void join_body(const JoinArgs& a) {
           S.mbk = min_bk16(S.BK);
           S.dirty = false;
           if constexpr (R == R32) sweep_segment32<SELF>(sm, cx, lane, FA, GA, S);
+        } else if constexpr (R == RW) {
+          static_assert(R != RW || !SYM, "the wide sweep has no symmetric variant");
+          WideState<R> S;
+          S.dirty = false;
+          double dfa[R], dga[R];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int64_t i = i0 + R * lane + r;
+            const bool in = i < a.nrows;
+            S.P[r] = head[r];
+            dfa[r] = in ? a.dfa[i] : 0.0;
+            dga[r] = in ? a.dga[i] : 0.0;
+            S.bKp[r] = kplus(sm.bK[r][lane]);
+          }
+          sweep_segment_w<R, SELF>(sm, cx, lane, dfa, dga, S);
         } else if constexpr (TSD_PIPE && !SYM) {
           PipeState<R> S;
           S.dirty = false;
@@ -1672,7 +1863,7 @@ constexpr int join_nreg() {
 }
 // two kernels around one body: the launch-bound budget, or a __maxnreg__ cap
 template <int R, bool SELF, bool F32, bool SYM>
-__global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_JOIN_MINB_SYM : TSD_JOIN_MINB)
+__global__ void __launch_bounds__(32 * WARPS, F32 ? TSD_JOIN_MINB32 : SYM ? TSD_JOIN_MINB_SYM : R == 16 ? TSD_JOIN_MINB_WIDE : TSD_JOIN_MINB)
     k_join(const JoinArgs a) {
   join_body<R, SELF, F32, SYM>(a);
 }
@@ -2147,7 +2338,7 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
   // TSD_SMEM_PAD (development): extra dynamic shared memory per CTA, to probe the
   // sweep's sensitivity to resident warps
   static const size_t smem_pad = getenv("TSD_SMEM_PAD") ? (size_t)atol(getenv("TSD_SMEM_PAD")) : 0;
-  const size_t smem_bytes = sizeof(WarpSmem<R>) * WARPS + smem_pad;
+  const size_t smem_bytes = sizeof(WarpSmem<R, (R == 16 && !F32)>) * WARPS + smem_pad;
   auto kern = [] {
     if constexpr (join_nreg<R, SELF, F32, SYM>() == 0)
       return k_join<R, SELF, F32, SYM>;
@@ -2827,6 +3018,16 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     if (bad == 0) return kOk;
     return sweep(in);
   }
+  // AB / dictionary join. The wide sweep (16 rows per lane) is an ablation
+  // build (-DTSD_WIDE_BUILD, then TSD_WIDE=1): measured equal on C4 (504 vs
+  // 500 ms at 12 instead of 16 resident warps) and slower on short joins
+#ifdef TSD_WIDE_BUILD
+  {
+    const char* we = getenv("TSD_WIDE");
+    const bool wide = we ? atoi(we) != 0 : TSD_WIDE_DEFAULT && in.rows.nwin >= (int64_t)TSD_WIDE_MIN_ROWS;
+    if (wide) return launch_join<RW, false, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
+  }
+#endif
   return launch_join<8, false, false, false>(in, d_best_c, d_best_j, arena, st, err, launches);
 }
 

@@ -1,6 +1,6 @@
 """Development tool: time library variants (tools/dev/abl_build.sh) on the
 same inputs and check that their profiles are bit-identical to the first.
-usage: python tools/dev/variants.py LIB1.so LIB2.so ... -- CFG ...
+usage: python tools/dev/variants.py LIB1.so[@ENV=VAL,...] LIB2.so ... -- CFG ...
 CFG = dict:NQ:NSEG:L:M[:PREC] | self:N:M[:EXCL]  (walk inputs, seeds 4 / 5)"""
 import json, os, subprocess, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -53,10 +53,14 @@ def main():
     libs, cfgs = a[:a.index("--")], a[a.index("--") + 1:]
     res = {}
     base = None
-    for lib in libs:
-        d = os.path.join("/tmp", "tsd_variants", os.path.basename(lib).replace(".so", ""))
+    for spec in libs:
+        lib, _, evs = spec.partition("@")
+        d = os.path.join("/tmp", "tsd_variants", os.path.basename(spec).replace(".so", "").replace("=", "_").replace(",", "_"))
         os.makedirs(d, exist_ok=True)
         env = dict(os.environ, TSD_LIB=os.path.abspath(lib))
+        for kv in filter(None, evs.split(",")):
+            env[kv.split("=")[0]] = kv.split("=")[1]
+        lib = spec
         r = subprocess.run([sys.executable, "-c", CHILD % (ROOT, cfgs, d)], env=env, capture_output=True, text=True)
         line = [l for l in r.stdout.splitlines() if l.startswith("RESULT ")]
         if not line:
@@ -72,6 +76,11 @@ def main():
                 fn = c.replace(":", "_") + ".npz"
                 x, y = np.load(os.path.join(base, fn)), np.load(os.path.join(d, fn))
                 same[c] = bool(np.array_equal(x["v"], y["v"]) and np.array_equal(x["i"], y["i"]))
+                if not same[c]:  # different plans restart the recurrence at other rows: report the distance
+                    fin = np.isfinite(x["v"]) & np.isfinite(y["v"])
+                    rel = float(np.max(np.abs(x["v"][fin] - y["v"][fin]) / np.maximum(x["v"][fin], 1e-300))) if fin.any() else 0.0
+                    same[c] = {"max_rel": rel, "index_mismatches": int(np.sum(x["i"] != y["i"])),
+                               "nonfinite_mismatch": int(np.sum(np.isfinite(x["v"]) != np.isfinite(y["v"])))}
         print(json.dumps({"lib": lib, "res": res[lib], "bitwise_equal_to_first": same}), flush=True)
 
 main()
