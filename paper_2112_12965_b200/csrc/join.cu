@@ -76,6 +76,9 @@ constexpr int T = 64;     // head / top-edge staging chunk (samples)
 #ifndef TSD_NREG32
 #define TSD_NREG32 0   // FP32 sweep
 #endif
+#ifndef TSD_NREG_WIDE
+#define TSD_NREG_WIDE 0  // wide FP64 sweep (ablation build)
+#endif
 #ifndef TSD_NREG_SYM
 #define TSD_NREG_SYM 0  // symmetric self-join sweep
 #endif
@@ -1063,10 +1066,8 @@ constexpr int RW = 16;
 template <int R>
 struct WideState {
   double P[R];    // slot r's covariance at the current column
-  double bKp[R];  // kplus(bestK)
-  int thr[R];     // hi(bKp * nmin) of the current threshold block
+  int thr[R];     // hi(kplus(bestK) * nmin) of the current threshold block (bests live in sm.bK only)
   double dfb, dgb, in, nmin;  // prefetched column data / incoming diagonal of the next column
-  bool dirty;
 };
 
 // warp vote over 16 slot tests "hi(cov) >= thr" (four 4-deep predicate chains)
@@ -1112,13 +1113,14 @@ __device__ __forceinline__ void sweep_block_w(WarpSmem<R, true>& sm, const Sweep
     if (GUARD && k >= n) break;
     if (u == 0) {  // column k opens a threshold block
       if (FIRST) S.nmin = ccur[0].w;
-      if (S.dirty) {
+      // thresholds straight from the bests in shared memory (no register copy
+      // of kplus(bestK): 32 registers the 14-warp budget does not have). A
+      // best <= 0 gives a product with the sign bit set (or +0): as unsigned
+      // it is >= 0x80000000, so the unsigned minimum turns it into INT_MIN
+      // (passes everything), exactly kplus's rule; +inf (inactive) never passes
 #pragma unroll
-        for (int r = 0; r < R; ++r) S.bKp[r] = kplus(sm.bK[r][lane]);
-        S.dirty = false;
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) S.thr[r] = __double2hiint(S.bKp[r] * S.nmin);
+      for (int r = 0; r < R; ++r)
+        S.thr[r] = (int)umin((unsigned)__double2hiint(sm.bK[r][lane] * S.nmin), 0x80000000u);
     }
     if (!(FIRST && u == 0)) {
       // lane 31 retires its bottom row of column k - 1 into the edge ring
@@ -1151,11 +1153,11 @@ __device__ __forceinline__ void sweep_block_w(WarpSmem<R, true>& sm, const Sweep
       const double invb = ccur[u].z;
       bool may = false;
 #pragma unroll
-      for (int r = 0; r < R; ++r) may |= S.P[r] * invb > S.bKp[r] || !(S.bKp[r] > 0.0);
+      for (int r = 0; r < R; ++r) may |= S.P[r] * invb > sm.bK[r][lane];
       if (__any_sync(0xffffffffu, may)) {
 #pragma unroll
         for (int r = 0; r < R; ++r) sm.slide[r * 32 + lane] = S.P[r];
-        S.dirty |= exact_update64<R, SELF>(sm, lane, cx.colbase + k, invb, cx.row0, cx.excl);
+        exact_update64<R, SELF>(sm, lane, cx.colbase + k, invb, cx.row0, cx.excl);
       }
     }
   }
@@ -1779,7 +1781,6 @@ __device__ __forceinline__ void join_body(const JoinArgs& a) {
         } else if constexpr (R == RW) {
           static_assert(R != RW || !SYM, "the wide sweep has no symmetric variant");
           WideState<R> S;
-          S.dirty = false;
           double dfa[R], dga[R];
 #pragma unroll
           for (int r = 0; r < R; ++r) {
@@ -1788,7 +1789,6 @@ __device__ __forceinline__ void join_body(const JoinArgs& a) {
             S.P[r] = head[r];
             dfa[r] = in ? a.dfa[i] : 0.0;
             dga[r] = in ? a.dga[i] : 0.0;
-            S.bKp[r] = kplus(sm.bK[r][lane]);
           }
           sweep_segment_w<R, SELF>(sm, cx, lane, dfa, dga, S);
         } else if constexpr (TSD_PIPE && !SYM) {
@@ -1859,7 +1859,7 @@ __device__ __forceinline__ void join_body(const JoinArgs& a) {
 
 template <int R, bool SELF, bool F32, bool SYM>
 constexpr int join_nreg() {
-  return F32 ? TSD_NREG32 : SYM ? TSD_NREG_SYM : TSD_NREG;
+  return F32 ? TSD_NREG32 : SYM ? TSD_NREG_SYM : R == 16 ? TSD_NREG_WIDE : TSD_NREG;
 }
 // two kernels around one body: the launch-bound budget, or a __maxnreg__ cap
 template <int R, bool SELF, bool F32, bool SYM>
