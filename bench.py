@@ -168,10 +168,20 @@ def run_reference(args):
     q = make_query(Q_SEED)
     threads = os.cpu_count() or 1
     vals = []
+    windows = args.ref_windows or (1 << 15)
     for s in range(args.warmup + args.steps):
-        r = cpu_reference_gcells(q, segs, threads, windows=args.ref_windows)
+        r = cpu_reference_gcells(q, segs, threads, windows=windows)
         if s >= args.warmup:
             vals.append(r["value"])
+        if s == 0 and not args.ref_windows:
+            # size the sample from the first warm-up step: the largest power of
+            # two up to 2^17 windows (BASELINE.md section 3's prefix) that keeps
+            # the whole run near 150 s; longer prefixes amortise the reference's
+            # per-call thread start-up, so they are the fairer figure
+            dt = (1 << 15) * N_SEG * (SEG_LEN - M + 1) / (r["value"] * 1e9)
+            rest = max(1, args.warmup + args.steps - 1)
+            while windows < (1 << 17) and rest * dt * (2 * windows / (1 << 15)) <= 150.0:
+                windows *= 2
     v = statistics.median(vals)
     cb = dict(r, value=v)
     line = {"impl": "reference", "metric": "AB-join distance cells/sec", "value": v, "unit": "GCell/s",
@@ -748,8 +758,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--ref-windows", type=int, default=1 << 15,
-                    help="query windows of C4 per reference-arm step (bounded sample)")
+    ap.add_argument("--ref-windows", type=int, default=0,
+                    help="query windows of C4 per reference-arm step (bounded sample); 0 = sized from the first "
+                         "warm-up step: 2^15 .. 2^17 windows so that the run takes about 150 s")
     ap.add_argument("--cpu-c3-windows", type=int, default=1 << 18,
                     help="query windows of C3 timed for its CPU baseline (0 = all, the full run)")
     ap.add_argument("--skip-configs", action="store_true", help="only the C4 headline (+ fp32, self-join) lines")
