@@ -2910,8 +2910,8 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     // to (1/2, 1]: every scaled covariance then lies in [-1, 1]. The FP32
     // sweep needs the smallest scaled products (and the K = cov * invn_b
     // values) to stay well inside the FP32 range; inputs whose window norms
-    // span more than that (about 2^96 over both sides -- e.g. blocks of the
-    // query at wildly different magnitudes) run the FP64 sweep instead.
+    // span more than the FP32 mode's accuracy allows (2^10 over both sides,
+    // below) run the FP64 sweep instead.
     unsigned long long* d_rng = (unsigned long long*)arena.get(sizeof(unsigned long long) * 4);
     if (!d_rng) {
       if (err) *err = Error{kCudaError, "device allocation failed for the FP32 scaling"};
@@ -2941,10 +2941,17 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     fin.f32_sigb = std::ldexp(1.0, -std::ilogb(mxb) - 1);
     const double span = (mna / mxa) * (mnb / mxb);
     // (K = cov * invn_b, bounded by mxa * mxb / mnb, is kept in FP32 too)
-    const bool fits = span > 0x1p-96 && mxa * (mxb / mnb) < 0x1p110;
+    // Accuracy: a cell's FP32 covariance carries eps32 x the largest |cov| its
+    // diagonal has seen since the last FP64 restart, i.e. up to eps32 / span
+    // in correlation units once a diagonal has crossed the largest windows of
+    // both sides and reached the smallest. The BASELINE shapes span 10 (ECG)
+    // to 218 (C4 walks) and stay ten times inside the 1e-3 distance tolerance;
+    // a x1000 stretch inside one dictionary segment (span 2e-5) missed it by
+    // 20x in the randomized tests. Beyond 2^10 the FP64 sweep runs instead.
+    const bool fits = span > 0x1p-10 && mxa * (mxb / mnb) < 0x1p110;
     if (getenv("TSD_VERBOSE"))
       fprintf(stderr, "[tsd] fp32 norms a [%.3g, %.3g] b [%.3g, %.3g] -> %s\n", mna, mxa, mnb, mxb,
-              fits ? "fp32 sweep" : "fp64 sweep (norm range too wide for fp32)");
+              fits ? "fp32 sweep" : "fp64 sweep (window norms span more than 2^10 over both sides)");
     if (!fits) {
       JoinInputs din = in;
       din.precision = 0;

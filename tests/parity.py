@@ -22,10 +22,17 @@ RHO = 1e-12
 TIE = 1e-9
 
 
-def check_profile(gv, gi, rv, ri, m, dist=None, fp32=False, label="", rho=RHO):
+def check_profile(gv, gi, rv, ri, m, dist=None, fp32=False, label="", rho=RHO, truth=False):
     """Returns a dict of statistics; raises AssertionError on a violation.
     `rho` bounds the correlation error (d^2 = 2m(1 - rho)) for rows whose
-    relative distance error exceeds REL; ties use the same bound."""
+    relative distance error exceeds REL; ties use the same bound.
+    `truth`: a row outside the tolerance of the REFERENCE value is judged
+    against the long-double distance dist(i, j) instead -- the reference's
+    whole-length diagonals carry more rounding than the kernel's restarted
+    ones (test_randomized_shapes_vs_oracle: reference 4e-8 relative off the
+    exact distance, GPU 1e-10). The GPU value must then be within the
+    tolerance of the exact distance of ITS neighbour, and that neighbour at
+    least as good as the reference's. Such rows are counted in the report."""
     gv, gi, rv, ri = map(np.asarray, (gv, gi, rv, ri))
     assert gv.shape == rv.shape and gi.shape == ri.shape, f"{label}: shape {gv.shape} vs {rv.shape}"
     inf_r = ~np.isfinite(rv)
@@ -37,6 +44,17 @@ def check_profile(gv, gi, rv, ri, m, dist=None, fp32=False, label="", rho=RHO):
         bad = dv > 1e-3
     else:
         bad = (dv > REL * rv[f]) & (np.abs(gv[f] ** 2 - rv[f] ** 2) > 2 * m * rho)
+    ref_off = 0
+    if truth and bad.any() and dist is not None and not fp32:
+        rows = np.nonzero(f)[0]
+        for k in np.nonzero(bad)[0]:
+            i = int(rows[k])
+            tg, tr = dist(i, int(gi[i])), dist(i, int(ri[i]))
+            ok_val = abs(gv[i] - tg) <= REL * tg or abs(gv[i] ** 2 - tg ** 2) <= 2 * m * rho
+            ok_nn = tg <= tr + max(TIE, REL * tr) or abs(tg * tg - tr * tr) <= 2 * m * rho
+            if ok_val and ok_nn:
+                bad[k] = False
+                ref_off += 1
     assert not bad.any(), (f"{label}: {bad.sum()} rows outside tolerance, worst |dd|={dv.max():.3g} "
                            f"at row {np.nonzero(f)[0][np.argmax(dv)]}")
     mism = np.nonzero(gi != ri)[0]
@@ -53,6 +71,8 @@ def check_profile(gv, gi, rv, ri, m, dist=None, fp32=False, label="", rho=RHO):
     fallback = 0 if fp32 else int(np.count_nonzero(dv > REL * rv[f]))
     out = {"label": label, "rows": int(gv.size), "max_rel": float(rel.max()) if rel.size else 0.0,
            "max_abs": float(dv.max()) if dv.size else 0.0, "ties": ties, "rho_fallback_rows": fallback}
+    if truth:
+        out["rows_judged_against_exact_distance"] = ref_off
     report(out)
     return out
 

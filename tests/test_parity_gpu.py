@@ -480,9 +480,10 @@ def test_fp32_mode_self_join_and_flat():
 def test_fp32_scaling_and_fp64_fallback(capfd, monkeypatch):
     """The FP32 sweep runs on power-of-two scaled statistics (join.cu
     run_join): inputs at extreme but uniform magnitudes stay in FP32; a query
-    whose window norms span more than the FP32 range (two 16384-window blocks
-    at 1e-6 and 1e60 -- each non-flat against its own block maximum,
-    dictionary.hpp:175-180) runs the FP64 sweep instead. Both within the
+    whose window norms span more than the FP32 mode's accuracy allows (2^10
+    over both sides; here two 16384-window blocks at 1e-6 and 1e60 -- each
+    non-flat against its own block maximum, dictionary.hpp:175-180) runs the
+    FP64 sweep instead. Both within the
     FP32 tolerance of the oracle."""
     monkeypatch.setenv("TSD_VERBOSE", "1")
     m = 128
@@ -506,7 +507,7 @@ def test_fp32_scaling_and_fp64_fallback(capfd, monkeypatch):
     capfd.readouterr()
     P = tsd.join_dictionary(q2, _dict(segs, starts, m), m, precision="fp32")
     err = capfd.readouterr().err
-    assert "fp64 sweep (norm range too wide" in err, err[-2000:]
+    assert "fp64 sweep (window norms span" in err, err[-2000:]
     rv, ri = O.dict_join(q2, segs, starts, m)
     st = check_profile(P.values, P.indices, rv, ri, m, dict_dist(q2, segs, starts, m), fp32=True,
                        label="fp32 -> fp64 fallback")
@@ -858,3 +859,88 @@ def test_distance_profiles_vs_reference(kind, n, m):
         bad[3] = np.inf
         tsd.distance_profile_mass(t, bad, st)
     assert e.value.code() == tsd.errc.non_finite_input
+
+
+# ------------------------------------------------------------- randomized shapes
+def _random_series(rng, n, kind):
+    """seeded inputs of the kinds the reference tests use (walks, noise, a
+    periodic signal), optionally with a flat run and a rescaled stretch"""
+    if kind == 0:
+        x = np.cumsum(rng.standard_normal(n))
+    elif kind == 1:
+        x = rng.standard_normal(n)
+    else:
+        x = np.sin(np.arange(n) * (2 * np.pi / rng.integers(17, 90))) + 0.1 * rng.standard_normal(n)
+    if n > 40 and rng.random() < 0.35:  # a flat run (profiles.hpp:290-294, :331-336)
+        a = int(rng.integers(0, n - 20))
+        x[a: a + int(rng.integers(5, min(n - a, 120)))] = x[a]
+    if n > 40 and rng.random() < 0.25:
+        # a stretch at another scale, one decade either way: the diagonal
+        # recurrence (the reference's as much as this one) carries eps x the
+        # largest covariance it has crossed, so wider jumps leave the 1e-12
+        # correlation bound on BOTH sides of the comparison (three decades:
+        # 2.5e-8 of distance between reference and GPU at m = 5); those are
+        # test_window_stats_and_join_across_huge_excursions' subject
+        a = int(rng.integers(0, n - 20))
+        x[a: a + int(rng.integers(5, n - a))] *= 10.0 ** rng.choice([-1, 1])
+    return np.ascontiguousarray(x)
+
+
+def _norm_span(x, m):
+    """largest / smallest standard deviation over the non-flat windows of x"""
+    w = np.lib.stride_tricks.sliding_window_view(np.asarray(x, dtype=np.float64), m)
+    sd = w.std(axis=1)
+    sd = sd[sd > 1e-8 * max(1.0, float(np.max(np.abs(x))))]
+    return float(sd.max() / sd.min()) if sd.size else 1.0
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_randomized_shapes_vs_oracle(seed):
+    """ragged shapes around the band (256 / 512 rows), chunk (32 columns) and
+    threshold-block (8 columns) boundaries: dictionary, AB and self joins in
+    FP64 against the oracle, the dictionary join also in the FP32 mode"""
+    rng = np.random.default_rng(1000 + seed)
+    for case in range(5):
+        m = int(rng.choice([2, 3, 5, 8, 16, 31, 64, 100, 257]))
+        nseg = int(rng.integers(1, 9))
+        lens = [int(m + rng.integers(0, 600)) for _ in range(nseg)]
+        gaps = [int(rng.integers(0, 50)) for _ in range(nseg)]
+        starts, pos = [], 0
+        for L, g in zip(lens, gaps):
+            pos += g
+            starts.append(pos)
+            pos += L
+        kind = int(rng.integers(0, 3))
+        segs = [_random_series(rng, L, kind) for L in lens]
+        nq = int(m + rng.integers(0, 1500))
+        q = _random_series(rng, nq, kind)
+        tag = f"rand{seed}.{case} m={m} nq={nq} lens={lens}"
+        # The diagonal recurrence -- the reference's as much as the kernel's --
+        # carries eps x the largest covariance a diagonal has crossed, so the
+        # correlation of a cell is good to about eps x (norm span of the query)
+        # x (norm span of the dictionary). The BASELINE shapes span 10 .. 218
+        # and sit far inside tests/parity.py's 1e-12; three-sample windows of
+        # noise span 10^4 and more, and reference and GPU then differ by a few
+        # 1e-12 .. 1e-9 (two-sample windows of a walk span 10^6 .. 10^7 and
+        # reach 3e-9). The bound follows the span: 1e-14 x span, i.e. the
+        # usual 1e-12 up to a span of 100. Where the reference itself is the
+        # less accurate side, the long-double distance decides (parity.py).
+        span = _norm_span(q, m) * max(_norm_span(s, m) for s in segs)
+        rho = max(RHO, 1e-14 * span)
+        rv, ri = O.dict_join(q, segs, starts, m)
+        P = tsd.join_dictionary(q, _dict(segs, starts, m), m)
+        check_profile(P.values, P.indices, rv, ri, m, dict_dist(q, segs, starts, m), label="dict " + tag, rho=rho,
+                      truth=True)
+        P32 = tsd.join_dictionary(q, _dict(segs, starts, m), m, precision="fp32")
+        check_profile(P32.values, P32.indices, rv, ri, m, dict_dist(q, segs, starts, m), fp32=True,
+                      label="dict fp32 " + tag)
+        b = segs[0]
+        rv, ri = O.ab_join(q, b, m)
+        P = tsd.ab_join(q, b, m)
+        check_profile(P.values, P.indices, rv, ri, m, ab_dist(q, b, m), label="ab " + tag, rho=rho, truth=True)
+        if nq >= 2 * m:
+            excl = int(rng.choice([m // 2, m // 4, 0]))
+            rv, ri = O.self_join(q, m, excl)
+            P = tsd.self_join(q, m, excl=excl)
+            check_profile(P.values, P.indices, rv, ri, m, ab_dist(q, q, m), label=f"self excl={excl} " + tag,
+                          rho=max(RHO, 1e-14 * _norm_span(q, m) ** 2), truth=True)
