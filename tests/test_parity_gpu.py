@@ -901,9 +901,10 @@ def test_randomized_shapes_vs_oracle(seed):
     FP64 against the oracle, the dictionary join also in the FP32 mode"""
     rng = np.random.default_rng(1000 + seed)
     for case in range(5):
+        big = 8 if case == 4 else 1  # the last case of a seed: several bands, tasks and column chunks
         m = int(rng.choice([2, 3, 5, 8, 16, 31, 64, 100, 257]))
         nseg = int(rng.integers(1, 9))
-        lens = [int(m + rng.integers(0, 600)) for _ in range(nseg)]
+        lens = [int(m + rng.integers(0, 600 * big)) for _ in range(nseg)]
         gaps = [int(rng.integers(0, 50)) for _ in range(nseg)]
         starts, pos = [], 0
         for L, g in zip(lens, gaps):
@@ -912,7 +913,7 @@ def test_randomized_shapes_vs_oracle(seed):
             pos += L
         kind = int(rng.integers(0, 3))
         segs = [_random_series(rng, L, kind) for L in lens]
-        nq = int(m + rng.integers(0, 1500))
+        nq = int(m + rng.integers(0, 1500 * big))
         q = _random_series(rng, nq, kind)
         tag = f"rand{seed}.{case} m={m} nq={nq} lens={lens}"
         # The diagonal recurrence -- the reference's as much as the kernel's --
@@ -944,3 +945,50 @@ def test_randomized_shapes_vs_oracle(seed):
             P = tsd.self_join(q, m, excl=excl)
             check_profile(P.values, P.indices, rv, ri, m, ab_dist(q, q, m), label=f"self excl={excl} " + tag,
                           rho=max(RHO, 1e-14 * _norm_span(q, m) ** 2), truth=True)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_randomized_batched_symmetric_and_sharded(monkeypatch, seed):
+    """the other device paths on ragged shapes: the batched dictionary join
+    (series of different lengths in one pass, seams between them), the forced
+    symmetric self-join with its coarse seeds, and the sharded self-join --
+    each against the oracle"""
+    rng = np.random.default_rng(2000 + seed)
+    for case in range(3):
+        m = int(rng.choice([4, 9, 16, 33, 64, 130]))
+        kind = int(rng.integers(0, 3))
+        nseg = int(rng.integers(1, 6))
+        lens = [int(m + rng.integers(0, 400)) for _ in range(nseg)]
+        starts, pos = [], 0
+        for L in lens:
+            pos += int(rng.integers(0, 30))
+            starts.append(pos)
+            pos += L
+        segs = [_random_series(rng, L, kind) for L in lens]
+        series = [_random_series(rng, int(m + rng.integers(0, 900)), kind) for _ in range(int(rng.integers(1, 8)))]
+        tag = f"rand-b{seed}.{case} m={m} series={[len(s) for s in series]} lens={lens}"
+        span_d = max(_norm_span(s, m) for s in segs)
+        outs = tsd.join_dictionary_batched(series, _dict(segs, starts, m), m)
+        assert len(outs) == len(series)
+        for k, q in enumerate(series):
+            rv, ri = O.dict_join(q, segs, starts, m)
+            check_profile(outs[k].values, outs[k].indices, rv, ri, m, dict_dist(q, segs, starts, m),
+                          label=f"batched series {k} " + tag, rho=max(RHO, 1e-14 * _norm_span(q, m) * span_d),
+                          truth=True)
+        # self-joins of a longer series: symmetric sweep forced, and three shards
+        t = _random_series(rng, int(2 * m + rng.integers(300, 6000)), kind)
+        excl = int(rng.choice([m // 2, m // 4, 0, 3 * m]))
+        if len(t) - m + 1 <= excl + 1:
+            excl = m // 2
+        rv, ri = O.self_join(t, m, excl)
+        rho = max(RHO, 1e-14 * _norm_span(t, m) ** 2)
+        monkeypatch.setenv("TSD_SYM", "1")
+        P = tsd.self_join(t, m, excl=excl)
+        check_profile(P.values, P.indices, rv, ri, m, ab_dist(t, t, m), label=f"sym self excl={excl} " + tag,
+                      rho=rho, truth=True)
+        monkeypatch.delenv("TSD_SYM")
+        parts = [tsd.self_join_partial(t, m, excl, s, 3) for s in range(3)]
+        c, j = tsd.merge_partials([p[0] for p in parts], [p[1] for p in parts])
+        S = tsd.self_join_finish(t, m, excl, c, j)
+        check_profile(S.values, S.indices, rv, ri, m, ab_dist(t, t, m), label=f"sharded self excl={excl} " + tag,
+                      rho=rho, truth=True)
