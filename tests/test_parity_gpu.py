@@ -992,3 +992,45 @@ def test_randomized_batched_symmetric_and_sharded(monkeypatch, seed):
         S = tsd.self_join_finish(t, m, excl, c, j)
         check_profile(S.values, S.indices, rv, ri, m, ab_dist(t, t, m), label=f"sharded self excl={excl} " + tag,
                       rho=rho, truth=True)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_randomized_learning_vs_reference(seed):
+    """learn_dictionary on random walks of random length, window, context
+    factor and stop rule against the unmodified reference run here
+    (oracle/_ref): identical picks and segments, e_max by the join's rule.
+    (Walk windows are distinctive, so the argmin of P - S has no near-ties;
+    the periodic golden case covers the tied kind.)"""
+    if not O.ref_available():
+        pytest.skip("the reference build (oracle/_ref) is not present")
+    rng = np.random.default_rng(3000 + seed)
+    for case in range(3):
+        n = int(rng.integers(1500, 9000))
+        m = int(rng.choice([16, 40, 64, 100]))
+        k = float(rng.choice([1.0, 1.5, 2.5]))
+        t = np.cumsum(rng.standard_normal(n))
+        rule = int(rng.integers(0, 3))
+        value = [float(rng.choice([0.5, 0.8, 0.95])), float(rng.integers(4 * m, n // 2)), float(rng.choice([0.5, 2.0]))][rule]
+        cfg = tsd.LearnConfig(m=m, k=k)
+        if rule == 0:
+            cfg.space_saving_target = value
+        elif rule == 1:
+            cfg.sample_budget = int(value)
+        else:
+            cfg.error_target = value
+        tag = f"rand-learn{seed}.{case} n={n} m={m} k={k} rule={rule} value={value}"
+        R = O.ref_learn_dictionary_full(t, m, k, rule, value)
+        D = tsd.learn_dictionary(t, cfg)
+        _dictionary_invariants(D, t)
+        assert D.core_starts == [int(x) for x in R["cores"]], f"{tag}: picks differ"
+        assert [s.start for s in D.segments] == [int(x) for x in R["starts"]], tag
+        assert [s.length() for s in D.segments] == [int(x) for x in R["lengths"]], tag
+        assert abs(D.space_saving - R["space_saving"]) <= 1e-12 and D.no_progress == bool(R["no_progress"]), tag
+        # e_max of a dictionary that covers (nearly) every window is a maximum
+        # over distances that are exactly 0: what remains is each side's
+        # recurrence rounding (rand-learn3.0: reference 1.7e-4 = 1e-9 of
+        # correlation over its 8600-step diagonals, GPU 2.2e-6), so near zero
+        # the two agree in correlation units (1e-8) rather than in distance
+        ok = abs(D.e_max - R["e_max"]) <= max(1e-8 * R["e_max"], 2e-5) or \
+            abs(D.e_max ** 2 - R["e_max"] ** 2) <= 2 * m * 1e-8
+        assert ok, f"{tag}: e_max {D.e_max} vs {R['e_max']}"
