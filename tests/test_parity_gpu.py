@@ -1034,3 +1034,59 @@ def test_randomized_learning_vs_reference(seed):
         ok = abs(D.e_max - R["e_max"]) <= max(1e-8 * R["e_max"], 2e-5) or \
             abs(D.e_max ** 2 - R["e_max"] ** 2) <= 2 * m * 1e-8
         assert ok, f"{tag}: e_max {D.e_max} vs {R['e_max']}"
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_randomized_stats_profiles_discords_vs_reference(seed):
+    """the remaining entry points on random inputs against the reference run
+    on the box: window statistics (1e-9, identical flat mask), the naive
+    distance profile (bit-identical), MASS (its own 1e-5) and find_discords
+    (identical starts, scores and certification, with ties and +inf rows)"""
+    if not O.ref_available():
+        pytest.skip("the reference build (oracle/_ref) is not present")
+    rng = np.random.default_rng(4000 + seed)
+    for case in range(4):
+        kind = int(rng.integers(0, 3))
+        m = int(rng.choice([2, 3, 7, 16, 50, 128, 300]))
+        n = int(m + rng.integers(1, 6000))
+        x = _random_series(rng, n, kind)
+        tag = f"rand-s{seed}.{case} n={n} m={m} kind={kind}"
+        st = tsd.compute_stats(x, m)
+        mu, sd, iv, fl = O.ref_compute_stats(x, m)
+        scale = max(1.0, float(np.max(np.abs(x))))
+        assert np.max(np.abs(st.means - mu)) <= 1e-9 * scale, tag
+        assert np.max(np.abs(st.stds - sd)) <= 1e-9 * scale, tag
+        assert np.array_equal(st.constant_mask, fl.astype(bool)), f"{tag}: flat masks differ at {np.nonzero(st.constant_mask != fl.astype(bool))[0][:5]}"
+        # relative accuracy against a long-double two-pass, not against the
+        # reference: its prefix-sum path lets a window's std be 1e-9 x the
+        # series scale off (series.hpp:130-142), which is 9e-7 relative for
+        # two-sample windows of a walk; the device statistics sit at 1e-16
+        nz = iv > 0
+        w = np.lib.stride_tricks.sliding_window_view(x.astype(np.longdouble), m)
+        sdx = np.sqrt(((w - w.mean(axis=1)[:, None]) ** 2).mean(axis=1))
+        assert np.all((st.invn > 0) == nz), tag
+        assert np.max(np.abs(st.stds[nz] - sdx[nz]) / sdx[nz]) <= 1e-12, tag
+        assert np.max(np.abs(st.invn[nz] * (sdx[nz] * np.sqrt(np.longdouble(m))) - 1.0)) <= 1e-12, tag
+        origin = int(rng.integers(0, n - m + 1))
+        q = x[origin:origin + m].copy()
+        nv = tsd.distance_profile_naive(x, q, st, origin)
+        rn = O.ref_distance_profile(x, q, m)
+        assert np.array_equal(nv.values, rn), f"{tag}: naive profile, {np.sum(nv.values != rn)} values differ"
+        if m >= 4:  # (MASS pads to a power of two; tiny windows are the naive form's job)
+            mv = tsd.distance_profile_mass(x, q, st, origin)
+            rm = O.ref_distance_profile(x, q, m, mass=True, origin=origin)
+            assert np.max(np.abs(mv.values - rm)) < 1e-5 * max(1.0, np.sqrt(2 * m)), tag
+        # discords of a random score profile with plateaus, ties and sentinels
+        cnt = int(rng.integers(1, 5000))
+        v = np.round(rng.random(cnt) * 8.0, int(rng.integers(0, 4)))
+        if cnt > 10:
+            v[rng.integers(0, cnt, 3)] = np.inf
+        md = int(rng.choice([2, 8, 64]))
+        e_max = float(rng.choice([0.0, 0.5, 3.0]))
+        top_k = int(rng.integers(1, 12))
+        got = tsd.find_discords(tsd.MatrixProfile(values=v, indices=np.zeros(cnt, dtype=np.int64), kind="ab", m=md),
+                                e_max, top_k)
+        rs, rsc, rce = O.ref_find_discords(v, md, e_max, top_k)
+        assert [g.start for g in got] == [int(a) for a in rs], f"{tag}: discord starts"
+        assert [g.score for g in got] == [float(a) for a in rsc], f"{tag}: discord scores"
+        assert [g.certified for g in got] == [bool(a) for a in rce], f"{tag}: discord certification"
