@@ -1090,3 +1090,44 @@ def test_randomized_stats_profiles_discords_vs_reference(seed):
         assert [g.start for g in got] == [int(a) for a in rs], f"{tag}: discord starts"
         assert [g.score for g in got] == [float(a) for a in rsc], f"{tag}: discord scores"
         assert [g.certified for g in got] == [bool(a) for a in rce], f"{tag}: discord certification"
+
+
+def test_concurrent_host_threads_are_deterministic():
+    """the entry points are re-entrant (SPEC: callable concurrently from
+    several host threads; per-thread stream, arena and plan caches): four
+    threads running different joins at once return exactly what each join
+    returns alone"""
+    import threading
+    rng = np.random.default_rng(77)
+    segs = [np.cumsum(rng.standard_normal(700)) for _ in range(6)]
+    starts = [900 * k for k in range(6)]
+    m = 64
+    D = _dict(segs, starts, m)
+    qs = [np.cumsum(rng.standard_normal(20000 + 997 * k)) for k in range(4)]
+    jobs = [
+        lambda k=0: tsd.join_dictionary(qs[0], D, m),
+        lambda k=1: tsd.ab_join(qs[1], segs[0], m),
+        lambda k=2: tsd.self_join(qs[2], m, excl=16),
+        lambda k=3: tsd.join_dictionary(qs[3], D, m, precision="fp32"),
+    ]
+    alone = [j() for j in jobs]
+    out = [[None] * 3 for _ in jobs]
+    errors = []
+
+    def work(k):
+        try:
+            for it in range(3):
+                out[k][it] = jobs[k]()
+        except Exception as e:  # surfaced below
+            errors.append((k, repr(e)))
+
+    threads = [threading.Thread(target=work, args=(k,)) for k in range(len(jobs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for k, ref in enumerate(alone):
+        for it in range(3):
+            assert np.array_equal(out[k][it].values, ref.values) and np.array_equal(out[k][it].indices, ref.indices), \
+                f"job {k}, iteration {it}: differs from the single-threaded result"
