@@ -228,7 +228,7 @@ int plan_join_dev(tsd_dict_plan* p, const double* d_q, const size_t* q_len, size
   if (!d_bc || !d_bj || !d_woff || !d_ooff) return fail(kCudaError, "device allocation failed for the join");
   CK(cudaMemcpyAsync(d_woff, woff.data(), sizeof(int64_t) * nser, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_ooff, ooff.data(), sizeof(int64_t) * nser, cudaMemcpyHostToDevice, st));
-  int launches = 5;  // stats kernels
+  int launches = window_stat_launches((int)m);  // stats kernels
   for (int e = 4; e < 8; ++e) in.ev[e - 4] = p->s.ev[e];
   CK(cudaEventRecord(p->s.ev[1], st));
   TRY(run_join(in, d_bc, d_bj, ar, st, &er, &launches));
@@ -456,7 +456,7 @@ static int single_join(const double* a, size_t na, const double* b, size_t nb, s
     float dm = 0.f, km = 0.f;
     cudaEventElapsedTime(&dm, tc.s.ev[0], tc.s.ev[1]);
     if (cudaEventElapsedTime(&km, tc.s.ev[6], tc.s.ev[7]) != cudaSuccess) km = 0.f;
-    t_last = LastJoin{dm, km, launches + 8};
+    t_last = LastJoin{dm, km, launches + 3 + window_stat_launches((int)m)};
   }
   phase("epilogue + outputs");
   return kOk;

@@ -3043,7 +3043,7 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     k_seed_cand<<<(unsigned)((ncoarse * 32 + 255) / 256), 256, 0, st>>>(in.xa, cnt, in.m, in.excl, f, in.rows.mu,
                                                                         in.rows.invn, in.rows.df, in.rows.dg,
                                                                         in.rows.flag, d_cbj, ncoarse, d_seed);
-    if (launches) *launches += 2 + 5;
+    if (launches) *launches += 2 + window_stat_launches(md);
     JoinInputs sin = in;
     sin.seed_corr = d_seed;
     const char* me = getenv("TSD_SEED_MARGIN");  // test hook: a negative margin forces the re-run guard

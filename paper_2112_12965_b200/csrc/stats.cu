@@ -10,8 +10,11 @@
 // 1e-8*max(1, max|x|) (series.hpp:75-77) is evaluated per threshold group
 // (one reference TimeSeries / 16384-window query block).
 //
-// Kernels (all HBM-bound):
-//   k_group_max     max|x| per group + first series with a non-finite sample
+// Kernels:
+//   k_group_max          max|x| per group + first series with a non-finite sample
+//   k_window_stats_tile  (default) everything else, fused: per-tile prefixes in
+//                        shared memory, all per-window arrays out
+// and, for windows too long for a tile (or TSD_STATS_TILE=0), the global scans:
 //   k_scan_partial  per-block double-double sums of x, x^2
 //   k_scan_blocks   exclusive scan of the block sums (one CTA)
 //   k_scan_apply    writes P1 = prefix(x), P2 = prefix(x^2) as double-double
@@ -19,6 +22,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "tsd_common.cuh"
 #include "tsd_internal.h"
@@ -209,6 +213,156 @@ __device__ __forceinline__ void window_moments(const double* __restrict__ x, con
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused tile form (the default while the tile's prefixes fit in shared memory):
+// one CTA takes kTileWin consecutive windows, forms the double-double prefix
+// sums of x and x^2 over JUST the samples those windows cover (tile + m
+// samples, in shared memory) and writes every per-window array from them. No
+// global prefix arrays and no scan kernels: the samples are read once per tile
+// (plus the m - 1 halo) and 41 B per window go out -- the algorithmic bytes of
+// against 8 + 2 x 32 B per sample written and read back by the
+// three-kernel scan. Window sums are differences of LOCAL prefixes (at most
+// kTileWin + m terms), so their absolute error is far below the global form's
+// and the two-pass fallback of window_moments triggers even more rarely; the
+// rounded means and variances are the same doubles (both forms carry ~1e-30).
+// ---------------------------------------------------------------------------
+constexpr int kTileThreads = 256;
+constexpr int kTilePer = 8;
+constexpr int kTileWin = kTileThreads * kTilePer;  // windows per CTA
+
+__device__ __forceinline__ void tile_moments(const double* __restrict__ x, const double2* __restrict__ Q1,
+                                             const double2* __restrict__ Q2, int64_t p, int loc, int m, double& mean,
+                                             double& var) {
+  const double md = (double)m;
+  const double2 a0 = Q1[loc], a1 = Q1[loc + m], b0 = Q2[loc], b1 = Q2[loc + m];
+  const dd w1 = dd_sub(dd{a1.x, a1.y}, dd{a0.x, a0.y});
+  const dd w2 = dd_sub(dd{b1.x, b1.y}, dd{b0.x, b0.y});
+  const dd mu = dd_div_d(w1, md);
+  const dd v = dd_div_d(dd_sub(w2, dd_mul(w1, mu)), md);
+  mean = mu.hi + mu.lo;
+  var = v.hi + v.lo;
+  if (var < 0.0) var = 0.0;
+  const double e2 = 0x1p-100 * (fabs(b1.x) + fabs(b0.x));
+  const double e1 = 0x1p-100 * (fabs(a1.x) + fabs(a0.x));
+  if (e2 > 1e-12 * md * var || e1 * e1 > 1e-24 * md * md * var) [[unlikely]] {
+    // (the same two compensated passes as window_moments, series.hpp:126-142)
+    dd s{0.0, 0.0};
+    for (int t = 0; t < m; ++t) s = dd_add(s, dd{x[p + t], 0.0});
+    const dd mu2 = dd_div_d(s, md);
+    dd q{0.0, 0.0};
+    for (int t = 0; t < m; ++t) {
+      const dd d = dd_sub(dd{x[p + t], 0.0}, mu2);
+      q = dd_add(q, dd_mul(d, d));
+    }
+    const dd v2 = dd_div_d(q, md);
+    mean = mu2.hi + mu2.lo;
+    var = v2.hi + v2.lo;
+    if (var < 0.0) var = 0.0;
+  }
+}
+
+__global__ void __launch_bounds__(kTileThreads)
+    k_window_stats_tile(const double* __restrict__ x, int64_t n, int64_t nwin, int m,
+                        const Group* __restrict__ groups, int ngroups, const unsigned long long* __restrict__ gmax,
+                        double* __restrict__ mu, double* __restrict__ sdo, double* __restrict__ invn,
+                        double* __restrict__ df, double* __restrict__ dg, uint8_t* __restrict__ flag) {
+  extern __shared__ double2 tile_q[];
+  __shared__ dd2 sh[32];
+  const int64_t p0 = (int64_t)blockIdx.x * kTileWin;
+  const int64_t sb = p0 > 0 ? p0 - 1 : 0;  // the window before the tile's first one feeds its dg
+  const int64_t se = p0 + kTileWin + m - 1 < n ? p0 + kTileWin + m - 1 : n;
+  const int len = (int)(se - sb);
+  double2* Q1 = tile_q;            // Q1[k] = sum of x[sb .. sb + k), k = 0 .. len
+  double2* Q2 = tile_q + len + 1;  // the same of x^2
+  const int per = (len + kTileThreads - 1) / kTileThreads;
+  const int k0 = threadIdx.x * per, k1 = k0 + per < len ? k0 + per : len;
+  dd2 acc{{0, 0}, {0, 0}};
+  for (int k = k0; k < k1; ++k) {
+    const double v = x[sb + k];
+    acc.a = dd_add(acc.a, dd{v, 0.0});
+    acc.b = dd_add(acc.b, two_prod(v, v));
+  }
+  dd2 run = block_scan_excl(acc, sh, nullptr);
+  if (threadIdx.x == 0) {
+    Q1[0] = make_double2(0.0, 0.0);
+    Q2[0] = make_double2(0.0, 0.0);
+  }
+  for (int k = k0; k < k1; ++k) {
+    const double v = x[sb + k];
+    run.a = dd_add(run.a, dd{v, 0.0});
+    run.b = dd_add(run.b, two_prod(v, v));
+    Q1[k + 1] = make_double2(run.a.hi, run.a.lo);
+    Q2[k + 1] = make_double2(run.b.hi, run.b.lo);
+  }
+  __syncthreads();
+  const double md = (double)m;
+  // the group of the tile's first window; windows are visited in increasing
+  // order, so the lookup only ever moves forward
+  int g = -1;
+  {
+    int lo = 0, hi = ngroups - 1;
+    const int64_t pf = p0 + threadIdx.x;
+    while (lo <= hi) {
+      const int mid = (lo + hi) >> 1;
+      if (groups[mid].wbeg <= pf) {
+        g = mid;
+        lo = mid + 1;
+      } else {
+        hi = mid - 1;
+      }
+    }
+  }
+  // phase 1: moments of the tile's windows (each once; the window before the
+  // tile by thread 0), means parked in shared memory for the neighbours' dg
+  double* smean = reinterpret_cast<double*>(tile_q + 2 * (len + 1));  // smean[i]: window p0 - 1 + i
+  double mymean[kTilePer];
+  if (threadIdx.x == 0 && p0 > 0) {
+    double mean, var;
+    tile_moments(x, Q1, Q2, p0 - 1, 0, m, mean, var);
+    smean[0] = mean;
+  }
+#pragma unroll
+  for (int k = 0; k < kTilePer; ++k) {
+    const int64_t p = p0 + threadIdx.x + (int64_t)kTileThreads * k;
+    mymean[k] = 0.0;
+    if (p >= nwin) continue;
+    while (g + 1 < ngroups && groups[g + 1].wbeg <= p) ++g;
+    double mean, var;
+    tile_moments(x, Q1, Q2, p, (int)(p - sb), m, mean, var);
+    const double sd = sqrt(var);
+    uint8_t f = 0;
+    double iv = 0.0;
+    if (g >= 0 && p < groups[g].wend) {
+      const double mx = __longlong_as_double((long long)gmax[g]);
+      const double eps = 1e-8 * (mx > 1.0 ? mx : 1.0);  // series.hpp:75-77
+      const bool flat = sd < eps;                        // series.hpp:145
+      f = flat ? 3 : 1;
+      iv = flat ? 0.0 : 1.0 / (sd * sqrt(md));           // series.hpp:147
+    }
+    mu[p] = mean;
+    if (sdo) sdo[p] = sd;
+    invn[p] = iv;
+    flag[p] = f;
+    mymean[k] = mean;
+    smean[threadIdx.x + kTileThreads * k + 1] = mean;
+  }
+  __syncthreads();
+  // phase 2: make_diffs (profiles.hpp:89-99) on the concatenated buffer
+#pragma unroll
+  for (int k = 0; k < kTilePer; ++k) {
+    const int64_t p = p0 + threadIdx.x + (int64_t)kTileThreads * k;
+    if (p >= nwin) continue;
+    double dfv = 0.0, dgv = 0.0;
+    if (p > 0) {
+      const double xin = x[p + m - 1], xout = x[p - 1];
+      dfv = 0.5 * (xin - xout);
+      dgv = (xin - mymean[k]) + (xout - smean[threadIdx.x + kTileThreads * k]);
+    }
+    df[p] = dfv;
+    dg[p] = dgv;
+  }
+}
+
 __global__ void k_window_stats(const double* __restrict__ x, const double2* __restrict__ P1,
                                const double2* __restrict__ P2, int64_t nwin, int m, const Group* __restrict__ groups,
                                int ngroups, const unsigned long long* __restrict__ gmax, double* __restrict__ mu,
@@ -268,6 +422,16 @@ __global__ void k_window_stats(const double* __restrict__ x, const double2* __re
     }                                                                         \
   } while (0)
 
+static bool stats_tile_fits(int m, size_t* bytes) {
+  // a tile's two prefix arrays and its window means in shared memory (m up to ~4000)
+  const size_t b = 2 * sizeof(double2) * ((size_t)kTileWin + (size_t)m + 2) + sizeof(double) * (kTileWin + 2);
+  if (bytes) *bytes = b;
+  static const bool tile_off = getenv("TSD_STATS_TILE") && atoi(getenv("TSD_STATS_TILE")) == 0;
+  return !tile_off && b <= (size_t)200 * 1024;
+}
+
+int window_stat_launches(int m) { return stats_tile_fits(m, nullptr) ? 2 : 5; }
+
 int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group>& groups, int nseries,
                     WindowArrays& out, Arena& arena, cudaStream_t st, int* bad_series, Error* err,
                     const int** d_bad_out) {
@@ -279,9 +443,11 @@ int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group
   Group* d_groups = (Group*)arena.get(sizeof(Group) * ng);
   unsigned long long* d_gmax = (unsigned long long*)arena.get(sizeof(unsigned long long) * ng);
   int* d_bad = (int*)arena.get(sizeof(int) * 4);
-  dd2* d_bs = (dd2*)arena.get(sizeof(dd2) * nblk);
-  double2* d_P1 = (double2*)arena.get(sizeof(double2) * (n + 1));
-  double2* d_P2 = (double2*)arena.get(sizeof(double2) * (n + 1));
+  size_t tile_smem = 0;
+  const bool tile = stats_tile_fits(m, &tile_smem);
+  dd2* d_bs = tile ? nullptr : (dd2*)arena.get(sizeof(dd2) * nblk);
+  double2* d_P1 = tile ? nullptr : (double2*)arena.get(sizeof(double2) * (n + 1));
+  double2* d_P2 = tile ? nullptr : (double2*)arena.get(sizeof(double2) * (n + 1));
   out.nwin = nwin;
   out.mu = (double*)arena.get(sizeof(double) * nwin);
   out.sd = (double*)arena.get(sizeof(double) * nwin);
@@ -289,8 +455,8 @@ int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group
   out.df = (double*)arena.get(sizeof(double) * nwin);
   out.dg = (double*)arena.get(sizeof(double) * nwin);
   out.flag = (uint8_t*)arena.get(nwin + 16);
-  if (!d_groups || !d_gmax || !d_bad || !d_bs || !d_P1 || !d_P2 || !out.mu || !out.sd || !out.invn || !out.df ||
-      !out.dg || !out.flag) {
+  if (!d_groups || !d_gmax || !d_bad || (!tile && (!d_bs || !d_P1 || !d_P2)) || !out.mu || !out.sd || !out.invn ||
+      !out.df || !out.dg || !out.flag) {
     if (err) *err = Error{kCudaError, "device allocation failed for window statistics"};
     return kCudaError;
   }
@@ -306,11 +472,22 @@ int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group
     if (gx < 1) gx = 1;
     k_group_max<<<dim3(gx, gy), 256, 0, st>>>(d_x, d_groups, ng, m, d_gmax, d_bad, gy0);
   }
-  k_scan_partial<<<(unsigned)nblk, kScanThreads, 0, st>>>(d_x, n, d_bs);
-  k_scan_blocks<<<1, 1024, 0, st>>>(d_bs, nblk);
-  k_scan_apply<<<(unsigned)nblk, kScanThreads, 0, st>>>(d_x, n, d_bs, d_P1, d_P2);
-  k_window_stats<<<(unsigned)((nwin + 255) / 256), 256, 0, st>>>(d_x, d_P1, d_P2, nwin, m, d_groups, ng, d_gmax,
-                                                                  out.mu, out.sd, out.invn, out.df, out.dg, out.flag);
+  if (tile) {
+    static std::atomic<bool> attr_set{false};
+    if (!attr_set.load()) {
+      CUDA_TRY(cudaFuncSetAttribute(k_window_stats_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_set.store(true);
+    }
+    k_window_stats_tile<<<(unsigned)((nwin + kTileWin - 1) / kTileWin), kTileThreads, tile_smem, st>>>(
+        d_x, n, nwin, m, d_groups, ng, d_gmax, out.mu, out.sd, out.invn, out.df, out.dg, out.flag);
+  } else {
+    k_scan_partial<<<(unsigned)nblk, kScanThreads, 0, st>>>(d_x, n, d_bs);
+    k_scan_blocks<<<1, 1024, 0, st>>>(d_bs, nblk);
+    k_scan_apply<<<(unsigned)nblk, kScanThreads, 0, st>>>(d_x, n, d_bs, d_P1, d_P2);
+    k_window_stats<<<(unsigned)((nwin + 255) / 256), 256, 0, st>>>(d_x, d_P1, d_P2, nwin, m, d_groups, ng, d_gmax,
+                                                                    out.mu, out.sd, out.invn, out.df, out.dg,
+                                                                    out.flag);
+  }
   CUDA_TRY(cudaGetLastError());
   if (d_bad_out) {  // the caller reads the non-finite flag after its own synchronisation
     *d_bad_out = d_bad;

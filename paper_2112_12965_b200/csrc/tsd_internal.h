@@ -96,6 +96,9 @@ bool device_free_bytes(size_t* free_bytes);
 // d_bad_out != nullptr: no host synchronisation; *d_bad_out receives the device
 // int the caller reads after its own synchronisation (0x7fffffff = all
 // finite, else the lowest series index holding a non-finite sample).
+// kernels one compute_windows call launches (2: group maxima + the fused tile
+// kernel; 5 with the global prefix scans, for windows too long for a tile)
+int window_stat_launches(int m);
 int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group>& groups, int nseries,
                     WindowArrays& out, Arena& arena, cudaStream_t st, int* bad_series, Error* err,
                     const int** d_bad_out = nullptr);

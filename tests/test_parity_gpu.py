@@ -1131,3 +1131,26 @@ def test_concurrent_host_threads_are_deterministic():
         for it in range(3):
             assert np.array_equal(out[k][it].values, ref.values) and np.array_equal(out[k][it].indices, ref.indices), \
                 f"job {k}, iteration {it}: differs from the single-threaded result"
+
+
+def test_window_stats_long_windows_take_the_scan_form():
+    """windows too long for a shared-memory tile (m > ~3800) go through the
+    global double-double prefix scans: same accuracy against a long-double
+    two-pass, same flat mask as the reference, and a join on top of them"""
+    rng = np.random.default_rng(5)
+    n, m = 40000, 5000
+    x = np.cumsum(rng.standard_normal(n))
+    x[12000:19000] = x[12000]  # flat windows too
+    st = tsd.compute_stats(x, m)
+    w = np.lib.stride_tricks.sliding_window_view(x.astype(np.longdouble), m)
+    sdx = np.sqrt(((w - w.mean(axis=1)[:, None]) ** 2).mean(axis=1))
+    nz = st.invn > 0
+    assert nz.any() and (~nz).any()
+    assert np.max(np.abs(st.stds[nz] - sdx[nz]) / sdx[nz]) <= 1e-12
+    assert np.max(np.abs(st.means - w.mean(axis=1))) <= 1e-12 * np.max(np.abs(x))
+    if O.ref_available():
+        assert np.array_equal(st.constant_mask, O.ref_compute_stats(x, m)[3].astype(bool))
+    b = np.cumsum(rng.standard_normal(9000))
+    P = tsd.ab_join(x[:11000], b, m)
+    rv, ri = O.ab_join(x[:11000], b, m)
+    check_profile(P.values, P.indices, rv, ri, m, ab_dist(x[:11000], b, m), label="long windows (scan statistics)")
