@@ -234,6 +234,7 @@ __device__ __forceinline__ void tile_moments(const double* __restrict__ x, const
                                              const double2* __restrict__ Q2, int64_t p, int loc, int m, double& mean,
                                              double& var) {
   const double md = (double)m;
+  TSD_CHECK(loc >= 0 && Q1 + loc + m < Q2);  // inside the tile's first prefix array (Q2 follows it)
   const double2 a0 = Q1[loc], a1 = Q1[loc + m], b0 = Q2[loc], b1 = Q2[loc + m];
   const dd w1 = dd_sub(dd{a1.x, a1.y}, dd{a0.x, a0.y});
   const dd w2 = dd_sub(dd{b1.x, b1.y}, dd{b0.x, b0.y});
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kTileThreads)
   const int64_t sb = p0 > 0 ? p0 - 1 : 0;  // the window before the tile's first one feeds its dg
   const int64_t se = p0 + kTileWin + m - 1 < n ? p0 + kTileWin + m - 1 : n;
   const int len = (int)(se - sb);
+  TSD_CHECK(len >= m && len <= kTileWin + m && se <= n);
   double2* Q1 = tile_q;            // Q1[k] = sum of x[sb .. sb + k), k = 0 .. len
   double2* Q2 = tile_q + len + 1;  // the same of x^2
   const int per = (len + kTileThreads - 1) / kTileThreads;
