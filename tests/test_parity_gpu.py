@@ -939,12 +939,17 @@ def test_randomized_shapes_vs_oracle(seed):
         rv, ri = O.ab_join(q, b, m)
         P = tsd.ab_join(q, b, m)
         check_profile(P.values, P.indices, rv, ri, m, ab_dist(q, b, m), label="ab " + tag, rho=rho, truth=True)
+        P32 = tsd.ab_join(q, b, m, precision="fp32")
+        check_profile(P32.values, P32.indices, rv, ri, m, ab_dist(q, b, m), fp32=True, label="ab fp32 " + tag)
         if nq >= 2 * m:
             excl = int(rng.choice([m // 2, m // 4, 0]))
             rv, ri = O.self_join(q, m, excl)
             P = tsd.self_join(q, m, excl=excl)
             check_profile(P.values, P.indices, rv, ri, m, ab_dist(q, q, m), label=f"self excl={excl} " + tag,
                           rho=max(RHO, 1e-14 * _norm_span(q, m) ** 2), truth=True)
+            P32 = tsd.self_join(q, m, excl=excl, precision="fp32")
+            check_profile(P32.values, P32.indices, rv, ri, m, ab_dist(q, q, m), fp32=True,
+                          label=f"self fp32 excl={excl} " + tag)
 
 
 @pytest.mark.parametrize("seed", range(4))
