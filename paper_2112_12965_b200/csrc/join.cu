@@ -1650,8 +1650,12 @@ __device__ __forceinline__ void join_body(const JoinArgs& a) {
           const int64_t i = i0 + R * lane + r;
           const double bk = sm.bK[r][lane];
           if (i < a.nrows && bk != kInf) {
+            // (cthr holds kplus() values: -0.0 means "no positive bound yet" and
+            // must not lift a row from -inf -- its best may be a negative
+            // correlation, e.g. with an exclusion zone that leaves only distant,
+            // anti-correlated windows)
             const double klb = a.cthr[i];
-            if (klb > bk) sm.bK[r][lane] = klb;
+            if (klb > 0.0 && klb > bk) sm.bK[r][lane] = klb;
           }
         }
       }

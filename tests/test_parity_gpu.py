@@ -894,7 +894,11 @@ def _norm_span(x, m):
     return float(sd.max() / sd.min()) if sd.size else 1.0
 
 
-@pytest.mark.parametrize("seed", range(8))
+# more seeds for a one-off hunt: TSD_FUZZ_SEEDS=N (each seed draws its own shapes)
+_FUZZ = int(os.environ.get("TSD_FUZZ_SEEDS", "0"))
+
+
+@pytest.mark.parametrize("seed", range(_FUZZ or 8))
 def test_randomized_shapes_vs_oracle(seed):
     """ragged shapes around the band (256 / 512 rows), chunk (32 columns) and
     threshold-block (8 columns) boundaries: dictionary, AB and self joins in
@@ -952,7 +956,7 @@ def test_randomized_shapes_vs_oracle(seed):
                           label=f"self fp32 excl={excl} " + tag)
 
 
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(_FUZZ or 4))
 def test_randomized_batched_symmetric_and_sharded(monkeypatch, seed):
     """the other device paths on ragged shapes: the batched dictionary join
     (series of different lengths in one pass, seams between them), the forced
@@ -999,7 +1003,7 @@ def test_randomized_batched_symmetric_and_sharded(monkeypatch, seed):
                       rho=rho, truth=True)
 
 
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(_FUZZ or 4))
 def test_randomized_learning_vs_reference(seed):
     """learn_dictionary on random walks of random length, window, context
     factor and stop rule against the unmodified reference run here
@@ -1041,7 +1045,7 @@ def test_randomized_learning_vs_reference(seed):
         assert ok, f"{tag}: e_max {D.e_max} vs {R['e_max']}"
 
 
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(_FUZZ or 4))
 def test_randomized_stats_profiles_discords_vs_reference(seed):
     """the remaining entry points on random inputs against the reference run
     on the box: window statistics (1e-9, identical flat mask), the naive
@@ -1159,3 +1163,27 @@ def test_window_stats_long_windows_take_the_scan_form():
     P = tsd.ab_join(x[:11000], b, m)
     rv, ri = O.ab_join(x[:11000], b, m)
     check_profile(P.values, P.indices, rv, ri, m, ab_dist(x[:11000], b, m), label="long windows (scan statistics)")
+
+
+@pytest.mark.parametrize("n,m,excl", [(715, 130, 130), (715, 130, 390), (1500, 64, 1000), (3000, 32, 2000)])
+def test_symmetric_self_join_wide_exclusion_negative_bests(monkeypatch, n, m, excl):
+    """with a wide exclusion zone only distant windows remain and a row's best
+    correlation is often negative. The symmetric sweep seeded its rows from
+    the column thresholds, whose "no bound yet" value -0.0 lifted them from
+    -inf: negative bests were never recorded (rows came back as (+inf, -1) or
+    with a worse neighbour). Found by the randomized test; the full-matrix
+    sweep was not affected."""
+    for seed in range(40):  # the first seeded walk some of whose best correlations are negative
+        t = np.cumsum(np.random.default_rng(1000 * seed + n + excl).standard_normal(n))
+        rv, ri = O.self_join(t, m, excl)
+        if np.any(rv[np.isfinite(rv)] > np.sqrt(2 * m)):
+            break
+    else:
+        pytest.fail("no walk with a negative best correlation")
+    monkeypatch.setenv("TSD_SYM", "1")
+    P = tsd.self_join(t, m, excl=excl)
+    check_profile(P.values, P.indices, rv, ri, m, ab_dist(t, t, m), label=f"sym wide excl={excl}", truth=True)
+    parts = [tsd.self_join_partial(t, m, excl, s, 2) for s in range(2)]
+    c, j = tsd.merge_partials([p[0] for p in parts], [p[1] for p in parts])
+    S = tsd.self_join_finish(t, m, excl, c, j)
+    assert np.array_equal(S.values, P.values) and np.array_equal(S.indices, P.indices)
