@@ -2952,10 +2952,14 @@ int run_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena& a
     // to 218 (C4 walks) and stay ten times inside the 1e-3 distance tolerance;
     // a x1000 stretch inside one dictionary segment (span 2e-5) missed it by
     // 20x in the randomized tests. Beyond 2^10 the FP64 sweep runs instead.
-    const bool fits = span > 0x1p-10 && mxa * (mxb / mnb) < 0x1p110;
+    // (windows of fewer than 8 samples gain nothing from FP32 and their
+    // correlations sit at +-1 by construction, where FP32 ranking is weakest)
+    const bool fits = span > 0x1p-10 && mxa * (mxb / mnb) < 0x1p110 && in.m >= 8;
     if (getenv("TSD_VERBOSE"))
       fprintf(stderr, "[tsd] fp32 norms a [%.3g, %.3g] b [%.3g, %.3g] -> %s\n", mna, mxa, mnb, mxb,
-              fits ? "fp32 sweep" : "fp64 sweep (window norms span more than 2^10 over both sides)");
+              fits ? "fp32 sweep"
+                   : in.m < 8 ? "fp64 sweep (windows shorter than 8 samples)"
+                              : "fp64 sweep (window norms span more than 2^10 over both sides)");
     if (!fits) {
       JoinInputs din = in;
       din.precision = 0;
