@@ -475,11 +475,8 @@ int compute_windows(const double* d_x, int64_t n, int m, const std::vector<Group
     k_group_max<<<dim3(gx, gy), 256, 0, st>>>(d_x, d_groups, ng, m, d_gmax, d_bad, gy0);
   }
   if (tile) {
-    static std::atomic<bool> attr_set{false};
-    if (!attr_set.load()) {
-      CUDA_TRY(cudaFuncSetAttribute(k_window_stats_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr_set.store(true);
-    }
+    // (per device, so set on every call like the join kernels' -- a process may drive several GPUs)
+    CUDA_TRY(cudaFuncSetAttribute(k_window_stats_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     k_window_stats_tile<<<(unsigned)((nwin + kTileWin - 1) / kTileWin), kTileThreads, tile_smem, st>>>(
         d_x, n, nwin, m, d_groups, ng, d_gmax, out.mu, out.sd, out.invn, out.df, out.dg, out.flag);
   } else {
