@@ -2346,8 +2346,19 @@ int launch_join(const JoinInputs& in, double* d_best_c, int64_t* d_best_j, Arena
     // the symmetric sweep takes 128 pieces (more, shorter tasks: self-joins
     // of 2^20-2^21 windows 0.5-3 % faster, 2^22 unchanged), AB joins 64
     const int64_t np64 = pn ? std::max<int64_t>(1, atoll(pn)) : (SYM ? 128 : 64);
-    const int64_t lmax =
-        std::max<int64_t>(pe ? atoll(pe) : (in.min_tasks > 0 ? 256 : 2048), (tot + np64 - 1) / np64);
+    // a join too small to give every resident warp a (band, segment) task is
+    // latency-bound on its longest sweep: cut its segments into 256-column
+    // pieces as well (C1, 64 bands x 8 segments of 413 columns: kernel 0.187 ->
+    // 0.122 ms; 128- and 64-column pieces measured 0.13-0.15 ms)
+    int nsm0 = 148;
+    {
+      int dev0 = 0;
+      cudaGetDevice(&dev0);
+      cudaDeviceGetAttribute(&nsm0, cudaDevAttrMultiProcessorCount, dev0);
+    }
+    const bool small = !SYM && (int64_t)((in.rows.nwin + H - 1) / H) * (int64_t)in.segs.size() < (int64_t)nsm0 * 16;
+    const int64_t lmax = std::max<int64_t>(pe ? atoll(pe) : ((in.min_tasks > 0 || small) ? 256 : 2048),
+                                           (tot + np64 - 1) / np64);
     for (const auto& s : in.segs) {
       const int64_t np = (s.ncol + lmax - 1) / lmax;
       if (np <= 1) {
