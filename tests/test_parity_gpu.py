@@ -981,13 +981,20 @@ def test_randomized_batched_symmetric_and_sharded(monkeypatch, seed):
         series = [_random_series(rng, int(m + rng.integers(0, 900)), kind) for _ in range(int(rng.integers(1, 8)))]
         tag = f"rand-b{seed}.{case} m={m} series={[len(s) for s in series]} lens={lens}"
         span_d = max(_norm_span(s, m) for s in segs)
+        # the batched join sweeps the CONCATENATED buffer (diagonals run through
+        # the seams, straddling windows are discarded), so a series' first rows
+        # inherit the rounding of the magnitudes its neighbour's diagonals
+        # crossed: the bound follows the norm span of the whole batch (a 2000-seed
+        # run: a series after one 7x larger, 8e-12 of correlation at its row 3)
+        sds = np.concatenate([np.lib.stride_tricks.sliding_window_view(q, m).std(axis=1) for q in series])
+        sds = sds[sds > 1e-8 * max(1.0, max(float(np.max(np.abs(q))) for q in series))]
+        span_b = float(sds.max() / sds.min()) if sds.size else 1.0
         outs = tsd.join_dictionary_batched(series, _dict(segs, starts, m), m)
         assert len(outs) == len(series)
         for k, q in enumerate(series):
             rv, ri = O.dict_join(q, segs, starts, m)
             check_profile(outs[k].values, outs[k].indices, rv, ri, m, dict_dist(q, segs, starts, m),
-                          label=f"batched series {k} " + tag, rho=max(RHO, 1e-14 * _norm_span(q, m) * span_d),
-                          truth=True)
+                          label=f"batched series {k} " + tag, rho=max(RHO, 1e-14 * span_b * span_d), truth=True)
         # self-joins of a longer series: symmetric sweep forced, and three shards
         t = _random_series(rng, int(2 * m + rng.integers(300, 6000)), kind)
         excl = int(rng.choice([m // 2, m // 4, 0, 3 * m]))
