@@ -45,13 +45,16 @@ def check_profile(gv, gi, rv, ri, m, dist=None, fp32=False, label="", rho=RHO, t
     else:
         bad = (dv > REL * rv[f]) & (np.abs(gv[f] ** 2 - rv[f] ** 2) > 2 * m * rho)
     ref_off = 0
-    if truth and bad.any() and dist is not None and not fp32:
+    if truth and bad.any() and dist is not None:
         rows = np.nonzero(f)[0]
         for k in np.nonzero(bad)[0]:
             i = int(rows[k])
             tg, tr = dist(i, int(gi[i])), dist(i, int(ri[i]))
-            ok_val = abs(gv[i] - tg) <= REL * tg or abs(gv[i] ** 2 - tg ** 2) <= 2 * m * rho
-            ok_nn = tg <= tr + max(TIE, REL * tr) or abs(tg * tg - tr * tr) <= 2 * m * rho
+            if fp32:  # the FP32 mode's absolute tolerance, against the exact distances
+                ok_val, ok_nn = abs(gv[i] - tg) <= 1e-3, tg <= tr + 1e-3
+            else:
+                ok_val = abs(gv[i] - tg) <= REL * tg or abs(gv[i] ** 2 - tg ** 2) <= 2 * m * rho
+                ok_nn = tg <= tr + max(TIE, REL * tr) or abs(tg * tg - tr * tr) <= 2 * m * rho
             if ok_val and ok_nn:
                 bad[k] = False
                 ref_off += 1

@@ -940,14 +940,15 @@ def test_randomized_shapes_vs_oracle(seed):
         if f32:
             P32 = tsd.join_dictionary(q, _dict(segs, starts, m), m, precision="fp32")
             check_profile(P32.values, P32.indices, rv, ri, m, dict_dist(q, segs, starts, m), fp32=True,
-                          label="dict fp32 " + tag)
+                          label="dict fp32 " + tag, truth=True)
         b = segs[0]
         rv, ri = O.ab_join(q, b, m)
         P = tsd.ab_join(q, b, m)
         check_profile(P.values, P.indices, rv, ri, m, ab_dist(q, b, m), label="ab " + tag, rho=rho, truth=True)
         if f32:
             P32 = tsd.ab_join(q, b, m, precision="fp32")
-            check_profile(P32.values, P32.indices, rv, ri, m, ab_dist(q, b, m), fp32=True, label="ab fp32 " + tag)
+            check_profile(P32.values, P32.indices, rv, ri, m, ab_dist(q, b, m), fp32=True, label="ab fp32 " + tag,
+                          truth=True)
         if nq >= 2 * m:
             excl = int(rng.choice([m // 2, m // 4, 0]))
             rv, ri = O.self_join(q, m, excl)
@@ -957,7 +958,7 @@ def test_randomized_shapes_vs_oracle(seed):
             if f32:
                 P32 = tsd.self_join(q, m, excl=excl, precision="fp32")
                 check_profile(P32.values, P32.indices, rv, ri, m, ab_dist(q, q, m), fp32=True,
-                              label=f"self fp32 excl={excl} " + tag)
+                              label=f"self fp32 excl={excl} " + tag, truth=True)
 
 
 @pytest.mark.parametrize("seed", range(_FUZZ or 4))
